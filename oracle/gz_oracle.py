@@ -1,0 +1,196 @@
+"""ctypes binding for the CPU oracle (oracle/gz_oracle.c).
+
+TEST INFRASTRUCTURE ONLY -- the parity checker.  Imported by tests/,
+__graft_entry__.smoke() and bench.py's CPU-baseline leg; never by the product
+package (paper_2405_19493_b200/), which must fail loudly without its CUDA
+library instead of falling back to this code.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libgzoracle.so")
+
+ALG = {"polar": 0, "ziggurat": 1, "modified-ziggurat": 2}
+SRC = {"lcg48": 0, "splitmix": 1}
+GUARD = 1_000_000  # samplers.py:27 LOOP_GUARD / engine.py:37 _GUARD
+GOLDEN_GAMMA = 0x9E3779B97F4A7C15
+MASK64 = (1 << 64) - 1
+
+
+class GzoTables(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int), ("r", ctypes.c_double), ("v", ctypes.c_double),
+                ("x", ctypes.c_double * 1025), ("ktab", ctypes.c_uint64 * 1024),
+                ("wtab", ctypes.c_double * 1024), ("ytab", ctypes.c_double * 1025)]
+
+
+def build():
+    subprocess.run(["make", "-s", "-C", HERE], check=True)
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            build()
+        L = ctypes.CDLL(LIB_PATH)
+        P = ctypes.c_void_p
+        i64 = ctypes.c_int64
+        L.gzo_build_tables.argtypes = [ctypes.c_int, ctypes.POINTER(GzoTables)]
+        L.gzo_fill_gaussians.argtypes = [ctypes.c_int, ctypes.c_int, P, i64, i64, i64, P, P, P, P, P, P, P,
+                                         i64, ctypes.c_int]
+        L.gzo_fill_u64.argtypes = [ctypes.c_int, i64, i64, i64, P, P, P]
+        L.gzo_mutate.argtypes = [P, i64, i64, i64, P, P, P, P, ctypes.c_int, i64, ctypes.c_int]
+        L.gzo_checksum.argtypes = [P, i64]
+        L.gzo_checksum.restype = ctypes.c_uint64
+        L.gzo_moments_accumulate.argtypes = [P, i64, P]
+        L.gzo_mix64.argtypes = [ctypes.c_uint64]
+        L.gzo_mix64.restype = ctypes.c_uint64
+        L.gzo_mix_gamma.argtypes = [ctypes.c_uint64]
+        L.gzo_mix_gamma.restype = ctypes.c_uint64
+        for f in ("gzo_exp", "gzo_log"):
+            getattr(L, f).argtypes = [ctypes.c_double]
+            getattr(L, f).restype = ctypes.c_double
+        L.gzo_pow.argtypes = [ctypes.c_double, ctypes.c_double]
+        L.gzo_pow.restype = ctypes.c_double
+        _lib = L
+    return _lib
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+
+
+class Tables:
+    """Oracle ziggurat tables (tables.py:107-131 restated in C)."""
+
+    def __init__(self, n):
+        self.raw = GzoTables()
+        st = lib().gzo_build_tables(int(n), ctypes.byref(self.raw))
+        if st == 2:
+            raise ValueError(f"layer count must be a power of two >= 8, got {n}")
+        if st != 0:
+            raise RuntimeError(f"table construction failed for n={n}")
+        self.n = n
+        self.r = self.raw.r
+        self.v = self.raw.v
+        self.x = np.ctypeslib.as_array(self.raw.x)[: n + 1].copy()
+        self.ktab = np.ctypeslib.as_array(self.raw.ktab)[:n].copy()
+        self.wtab = np.ctypeslib.as_array(self.raw.wtab)[:n].copy()
+        self.ytab = np.ctypeslib.as_array(self.raw.ytab)[: n + 1].copy()
+
+
+_TABLES = {}
+
+
+def tables(n):
+    if n not in _TABLES:
+        _TABLES[n] = Tables(n)
+    return _TABLES[n]
+
+
+def default_layers(alg):
+    return 256 if alg == "modified-ziggurat" else 128
+
+
+def fill_gaussians(alg, source, states, n_per, spare=None, has=None, layers=None, guard=GUARD,
+                   nthreads=0):
+    """Multi-stream fill.  states: uint64[n] (lcg48) or uint64[n, 2] (splitmix).
+    Returns (out[n, n_per], states_out, spare_out, has_out, status)."""
+    states = np.ascontiguousarray(states, dtype=np.uint64)
+    n = states.shape[0]
+    out = np.zeros((n, n_per), dtype=np.float64)
+    st_out = np.empty_like(states)
+    t = None if alg == "polar" else tables(layers or default_layers(alg))
+    spare_out = np.zeros(n) if alg == "polar" else None
+    has_out = np.zeros(n, dtype=np.uint8) if alg == "polar" else None
+    if spare is not None:
+        spare = np.ascontiguousarray(spare, dtype=np.float64)
+        has = np.ascontiguousarray(has, dtype=np.uint8)
+    status = lib().gzo_fill_gaussians(ALG[alg], SRC[source], None if t is None else ctypes.byref(t.raw), n,
+                                      n_per, n_per, _p(states), _p(st_out), _p(spare), _p(has),
+                                      _p(spare_out), _p(has_out), _p(out), guard, nthreads)
+    return out, st_out, spare_out, has_out, status
+
+
+def fill_u64(source, states, n_per):
+    states = np.ascontiguousarray(states, dtype=np.uint64)
+    n = states.shape[0]
+    out = np.zeros((n, n_per), dtype=np.uint64)
+    st_out = np.empty_like(states)
+    lib().gzo_fill_u64(SRC[source], n, n_per, n_per, _p(states), _p(st_out), _p(out))
+    return out, st_out
+
+
+def mutate(states, x, sigma, generations, guard=GUARD, nthreads=0):
+    """x (n_ind, n_genes) float64 updated in place; states uint64[n, 2] (splitmix)."""
+    states = np.ascontiguousarray(states, dtype=np.uint64)
+    st_out = np.empty_like(states)
+    sigma = np.ascontiguousarray(sigma, dtype=np.float64)
+    n_ind, n_genes = x.shape
+    status = lib().gzo_mutate(ctypes.byref(tables(128).raw), n_ind, n_genes, n_genes, _p(states), _p(st_out),
+                              _p(x), _p(sigma), generations, guard, nthreads)
+    return st_out, status
+
+
+def checksum(buf):
+    buf = np.ascontiguousarray(buf, dtype=np.float64).reshape(-1)
+    return int(lib().gzo_checksum(_p(buf), buf.size))
+
+
+def moments_accumulate(xs, acc=None):
+    xs = np.ascontiguousarray(xs, dtype=np.float64).reshape(-1)
+    acc = np.zeros(5) if acc is None else acc
+    lib().gzo_moments_accumulate(_p(xs), xs.size, _p(acc))
+    return acc
+
+
+def moments_summary(acc):
+    """stats.py:249-258 from the accumulated (n, mean, m2, m3, m4)."""
+    import math
+    n, mean, m2, m3, m4 = acc
+    n = int(n)
+    variance = m2 / (n - 1)
+    if m2 == 0.0:
+        return n, mean, variance, 0.0, 0.0
+    skew = math.sqrt(float(n)) * m3 / m2 ** 1.5
+    kurt = n * m4 / (m2 * m2) - 3.0
+    return n, mean, variance, skew, kurt
+
+
+# ---- seeding conventions of the five configs ----
+
+def mix64(z):
+    return int(lib().gzo_mix64(z & MASK64))
+
+
+def lcg_state(seed):
+    return ((seed ^ 0x5DEECE66D) & ((1 << 48) - 1))
+
+
+def sm_output_seed(master, i):
+    return mix64((master + (i + 1) * GOLDEN_GAMMA) & MASK64)
+
+
+def config_states(cfg, ids):
+    """Initial per-stream states of config `cfg` for the given stream ids."""
+    ids = [int(i) for i in ids]
+    if cfg == "c1":
+        return np.array([[sm_output_seed(42, i), GOLDEN_GAMMA] for i in ids], dtype=np.uint64)
+    if cfg == "c2":
+        return np.array([lcg_state(7 + i) for i in ids], dtype=np.uint64)
+    if cfg == "c3":
+        return np.array([[sm_output_seed(1234, i), GOLDEN_GAMMA] for i in ids], dtype=np.uint64)
+    if cfg == "c4":
+        return np.array([lcg_state(99 + i) for i in ids], dtype=np.uint64)
+    if cfg == "c5":
+        return np.array([[i ^ 0xC0FFEE, GOLDEN_GAMMA] for i in ids], dtype=np.uint64)
+    raise ValueError(cfg)
