@@ -59,6 +59,8 @@ def lib():
         for f in ("gzo_exp", "gzo_log"):
             getattr(L, f).argtypes = [ctypes.c_double]
             getattr(L, f).restype = ctypes.c_double
+        L.gzo_libm_mismatches.argtypes = [ctypes.c_int, P, P, i64, ctypes.POINTER(ctypes.c_int64)]
+        L.gzo_libm_mismatches.restype = ctypes.c_int64
         L.gzo_pow.argtypes = [ctypes.c_double, ctypes.c_double]
         L.gzo_pow.restype = ctypes.c_double
         _lib = L
@@ -139,6 +141,28 @@ def mutate(states, x, sigma, generations, guard=GUARD, nthreads=0):
     status = lib().gzo_mutate(ctypes.byref(tables(128).raw), n_ind, n_genes, n_genes, _p(states), _p(st_out),
                               _p(x), _p(sigma), generations, guard, nthreads)
     return st_out, status
+
+
+def libm_mismatches(fn, xs, got):
+    """(count, first index) of got[k] != libm exp/log(xs[k]) bitwise (fn 0 exp, 1 log)."""
+    xs = np.ascontiguousarray(xs, dtype=np.float64)
+    got = np.ascontiguousarray(got, dtype=np.float64)
+    first = ctypes.c_int64()
+    bad = lib().gzo_libm_mismatches(fn, _p(xs), _p(got), xs.size, ctypes.byref(first))
+    return int(bad), int(first.value)
+
+
+def sweep_inputs(fn, n, seed):
+    """Inputs for the exp/log sweeps: the samplers' domains plus raw bit patterns."""
+    rng = np.random.default_rng(seed)
+    raw = rng.integers(0, 2 ** 64 - 1, n // 4, dtype=np.uint64, endpoint=True).view(np.float64)
+    if fn == 0:  # wedge test argument -0.5*x*x, x < r(256) = 3.654...
+        dom = -0.5 * (3.7 * rng.random(n)) ** 2
+    else:        # tail uniforms (53-bit grid) and polar s in (0, 1)
+        grid = rng.integers(1, 2 ** 53, n // 2, dtype=np.uint64).astype(np.float64) * 2.0 ** -53
+        dom = np.concatenate([grid, rng.random(n - n // 2)])
+        raw = np.abs(raw)
+    return np.concatenate([dom, raw])
 
 
 def checksum(buf):

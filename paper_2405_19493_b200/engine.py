@@ -1,0 +1,200 @@
+"""Batch engine: the drop-in for the reference's engine.py, on the B200.
+
+`fill_gaussians(sampler, source, out)` and `fill_u64(source, out)` keep the
+signatures and state write-back of /root/reference/pkg/src/gausszig/engine.py
+(fill_u64 224-232, fill_gaussians 235-270, supports 199-201, available 46-47,
+warm_up 273-281): the source's `state` and the polar sampler's `spare` are read
+before the call and written back after it, so batch calls and per-call calls
+interleave exactly as in the reference.
+
+`out` may be a numpy array (host memory: the call copies the stream state in,
+generates on the GPU and copies the deviates back -- gz_fill_gaussians_host)
+or a CUDA torch tensor (generated in place -- gz_fill_gaussians).
+
+Differences by design: there is no CPU fallback.  A source without a kernel
+(ScriptedSource) raises TypeError instead of running the per-call Python loop,
+and without libgzb200.so or a CUDA device every call raises EngineUnavailable.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from ._lib import DEFAULT_GUARD, EngineUnavailable, RejectionLoopExceeded, check
+from .samplers import GaussianSampler, ModifiedZigguratSampler, PolarSampler, ZigguratSampler
+from .sources import Lcg48, SplitMix64, UniformSource, make_source
+from .tables import ZigguratTables
+
+__all__ = ["available", "supports", "fill_u64", "fill_gaussians", "warm_up", "table_slot", "EngineUnavailable",
+           "RejectionLoopExceeded"]
+
+
+def _ptr(a):
+    return ctypes.c_void_p(a.ctypes.data) if isinstance(a, np.ndarray) else ctypes.c_void_p(a.data_ptr())
+
+
+def available() -> bool:
+    """True when libgzb200.so loads and a CUDA device is visible."""
+    try:
+        _lib.load()
+        return True
+    except (EngineUnavailable, OSError):
+        return False
+
+
+def supports(source: UniformSource) -> bool:
+    """Whether a device kernel exists for this source (engine.py:199-201)."""
+    return isinstance(source, (Lcg48, SplitMix64)) and available()
+
+
+# ---- table slots --------------------------------------------------------------
+
+_slots: dict = {}     # (device, id(tables)) -> (slot, tables)
+_next_slot: dict = {}
+
+
+def _current_device() -> int:
+    try:
+        import torch
+
+        return torch.cuda.current_device() if torch.cuda.is_available() else 0
+    except ImportError:  # pragma: no cover
+        return 0
+
+
+def table_slot(tables: ZigguratTables) -> int:
+    """Device table slot holding `tables` (uploaded on first use; replaces the
+    lru_cache'd _table_arrays of engine.py:216-221)."""
+    L = _lib.load()
+    dev = _current_device()
+    key = (dev, id(tables))
+    hit = _slots.get(key)
+    if hit is not None and hit[1] is tables:
+        return hit[0]
+    slot = _next_slot.get(dev, 0)
+    if slot >= 16:  # recycle: drop every slot of this device
+        for k in [k for k in _slots if k[0] == dev]:
+            del _slots[k]
+        slot = 0
+    _next_slot[dev] = slot + 1
+    k = np.ascontiguousarray(tables.ktab, dtype=np.uint64)
+    w = np.ascontiguousarray(tables.wtab, dtype=np.float64)
+    y = np.ascontiguousarray(tables.ytab, dtype=np.float64)
+    check(L.gz_tables_upload(slot, tables.n, _ptr(k), _ptr(w), _ptr(y), tables.r))
+    _slots[key] = (slot, tables)
+    return slot
+
+
+def _alg_of(sampler: GaussianSampler) -> int:
+    if isinstance(sampler, PolarSampler):
+        return _lib.ALG["polar"]
+    if isinstance(sampler, ModifiedZigguratSampler):
+        return _lib.ALG["modified-ziggurat"]
+    if isinstance(sampler, ZigguratSampler):
+        return _lib.ALG["ziggurat"]
+    raise TypeError(f"no engine kernel for sampler {getattr(sampler, 'algorithm_id', sampler)!r}")
+
+
+def _state_words(source: UniformSource) -> np.ndarray:
+    """engine.py:204-209 `_state_array`."""
+    if isinstance(source, Lcg48):
+        return np.array([source.state], dtype=np.uint64)
+    if isinstance(source, SplitMix64):
+        return np.array([source.state, source.gamma], dtype=np.uint64)
+    raise TypeError(f"no engine support for source {source.source_id!r} (the B200 engine has no CPU fallback)")
+
+
+def _is_cuda_tensor(out) -> bool:
+    return hasattr(out, "is_cuda") and bool(out.is_cuda)
+
+
+def fill_u64(source: UniformSource, out) -> None:
+    """Fill `out` (uint64, 1-D) with draws, advancing the source in place."""
+    L = _lib.load()
+    st = _state_words(source)
+    src = _lib.SRC[source.source_id]
+    if _is_cuda_tensor(out):
+        import torch
+
+        if out.dim() != 1 or not out.is_contiguous() or out.element_size() != 8:
+            raise ValueError("out must be a contiguous 1-D 64-bit CUDA tensor")
+        d_st = torch.from_numpy(st.view(np.int64)).to(out.device)
+        s = torch.cuda.current_stream(out.device).cuda_stream
+        check(L.gz_fill_u64(src, 1, out.numel(), out.numel(), _ptr(d_st), _ptr(d_st), _ptr(out), s))
+        check(L.gz_stream_check(s))
+        st = d_st.cpu().numpy().view(np.uint64)
+    else:
+        import torch
+
+        buf = np.ascontiguousarray(out) if isinstance(out, np.ndarray) else np.asarray(out)
+        if buf.dtype != np.uint64 or buf.ndim != 1:
+            raise ValueError("out must be a 1-D uint64 array")
+        d_st = torch.from_numpy(st.view(np.int64)).cuda()
+        d_out = torch.empty(buf.shape[0], dtype=torch.int64, device="cuda")
+        s = torch.cuda.current_stream().cuda_stream
+        check(L.gz_fill_u64(src, 1, buf.shape[0], buf.shape[0], _ptr(d_st), _ptr(d_st), _ptr(d_out), s))
+        check(L.gz_stream_check(s))
+        buf[...] = d_out.cpu().numpy().view(np.uint64)
+        if buf is not out:
+            out[...] = buf
+        st = d_st.cpu().numpy().view(np.uint64)
+    source.state = int(st[0])
+
+
+def fill_gaussians(sampler: GaussianSampler, source: UniformSource, out, guard: int = DEFAULT_GUARD) -> None:
+    """Fill `out` (float64, 1-D) with deviates, advancing sampler and source
+    state exactly as `sampler.next_gaussian(source)` called len(out) times would."""
+    L = _lib.load()
+    alg = _alg_of(sampler)
+    st = _state_words(source)
+    src = _lib.SRC[source.source_id]
+    slot = 0 if alg == 0 else table_slot(sampler.tables)
+    polar = alg == 0
+    spare_in = np.array([sampler.spare if polar and sampler.spare is not None else 0.0])
+    has_in = np.array([1 if polar and sampler.spare is not None else 0], dtype=np.uint8)
+    spare_out = np.zeros(1)
+    has_out = np.zeros(1, dtype=np.uint8)
+    if _is_cuda_tensor(out):
+        import torch
+
+        if out.dim() != 1 or not out.is_contiguous() or out.dtype != torch.float64:
+            raise ValueError("out must be a contiguous 1-D float64 CUDA tensor")
+        dev = out.device
+        d_st = torch.from_numpy(st.view(np.int64)).to(dev)
+        d_sp = torch.from_numpy(spare_in).to(dev)
+        d_hs = torch.from_numpy(has_in).to(dev)
+        d_spo = torch.zeros(1, dtype=torch.float64, device=dev)
+        d_hso = torch.zeros(1, dtype=torch.uint8, device=dev)
+        s = torch.cuda.current_stream(dev).cuda_stream
+        n = out.numel()
+        check(L.gz_fill_gaussians(alg, src, slot, 1, n, n, _ptr(d_st), _ptr(d_st),
+                                  _ptr(d_sp) if polar else None, _ptr(d_hs) if polar else None,
+                                  _ptr(d_spo) if polar else None, _ptr(d_hso) if polar else None,
+                                  _ptr(out), None, None, guard, s))
+        check(L.gz_stream_check(s))
+        st = d_st.cpu().numpy().view(np.uint64)
+        spare_out = d_spo.cpu().numpy()
+        has_out = d_hso.cpu().numpy()
+    else:
+        buf = out if (isinstance(out, np.ndarray) and out.dtype == np.float64 and out.ndim == 1
+                      and out.flags.c_contiguous) else np.empty(len(out), dtype=np.float64)
+        st_out = np.empty_like(st)
+        check(L.gz_fill_gaussians_host(alg, src, slot, 1, buf.shape[0], _ptr(st), _ptr(st_out),
+                                       _ptr(spare_in) if polar else None, _ptr(has_in) if polar else None,
+                                       _ptr(spare_out) if polar else None, _ptr(has_out) if polar else None,
+                                       _ptr(buf), None, guard))
+        if buf is not out:
+            out[...] = buf
+        st = st_out
+    source.state = int(st[0])
+    if polar:
+        sampler.spare = float(spare_out[0]) if has_out[0] else None
+
+
+def warm_up(sampler: GaussianSampler, source_id: str) -> None:
+    """Upload tables and run one small fill so a timed region sees no first-use cost."""
+    if not available():
+        return
+    fill_gaussians(sampler, make_source(source_id, 0), np.empty(64))

@@ -1,0 +1,372 @@
+"""Parity of the CUDA engine with the reference (golden fixtures) and the CPU
+oracle, bit for bit.  Needs a B200: run with `pytest -m gpu`.
+
+Every test drives the product through its public API (engine.fill_gaussians /
+fill_u64 with numpy or CUDA tensors, streams.*), i.e. through the C ABI of
+libgzb200.so; the oracle (oracle/gz_oracle.c) and the golden fixtures
+(tests/golden/golden.json, made by importing the reference) are the checkers.
+"""
+import hashlib
+import zlib
+
+import numpy as np
+import pytest
+
+from conftest import f64_to_hex, xor_hex
+
+torch = pytest.importorskip("torch")
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a CUDA device")]
+
+from oracle import gz_oracle as O  # noqa: E402
+import paper_2405_19493_b200 as gz  # noqa: E402
+from paper_2405_19493_b200 import engine, streams  # noqa: E402
+
+DEV = "cuda"
+PAIRINGS = [(s, a) for s in ("lcg48", "splitmix") for a in ("polar", "ziggurat", "modified-ziggurat")]
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def u64(t):
+    return t.cpu().numpy().view(np.uint64)
+
+
+def bits_equal(a, b):
+    return np.array_equal(np.ascontiguousarray(a).view(np.uint64), np.ascontiguousarray(b).view(np.uint64))
+
+
+def spare_hex(sampler):
+    return None if sampler.spare is None else f64_to_hex(np.array([sampler.spare]))[0]
+
+
+def dev_states(source, states_np):
+    return torch.from_numpy(np.ascontiguousarray(states_np, dtype=np.uint64).view(np.int64)).to(DEV)
+
+
+# ---- reference-facing single-stream API ------------------------------------
+
+@pytest.mark.parametrize("idx", range(6))
+def test_six_pairings_300k_host_path(idx, golden):
+    """tests/test_engine.py:16-28 through engine.fill_gaussians with a numpy out."""
+    g = golden["pairings"][idx]
+    smp = gz.make_sampler(g["sampler"])
+    src = gz.make_source(g["source"], g["seed"])
+    buf = np.empty(g["n"])
+    engine.fill_gaussians(smp, src, buf)
+    assert f64_to_hex(buf[:16]) == g["first"]
+    assert sha(buf) == g["sha256"]
+    assert "%016x" % src.state == g["state"]
+    if g["sampler"] == "polar":
+        assert spare_hex(smp) == g["spare"]
+
+
+@pytest.mark.parametrize("idx", range(6))
+def test_six_pairings_300k_device_tensor(idx, golden):
+    g = golden["pairings"][idx]
+    smp = gz.make_sampler(g["sampler"])
+    src = gz.make_source(g["source"], g["seed"])
+    out = torch.empty(g["n"], dtype=torch.float64, device=DEV)
+    engine.fill_gaussians(smp, src, out)
+    assert sha(out.cpu().numpy()) == g["sha256"]
+    assert "%016x" % src.state == g["state"]
+    if g["sampler"] == "polar":
+        assert spare_hex(smp) == g["spare"]
+
+
+def test_small_and_edge_sizes(golden):
+    for g in golden["small"]:
+        smp = gz.make_sampler(g["sampler"])
+        src = gz.make_source(g["source"], int(g["seed"], 16))
+        buf = np.empty(g["n"])
+        engine.fill_gaussians(smp, src, buf)
+        assert f64_to_hex(buf) == g["out"], (g["source"], g["sampler"], g["n"])
+        assert "%016x" % src.state == g["state"]
+        if g["sampler"] == "polar":
+            assert spare_hex(smp) == g["spare"]
+
+
+def test_polar_spare_carries_across_batches(golden):
+    """tests/test_engine.py:58-71."""
+    g = golden["polar_chunks"]
+    smp = gz.make_sampler("polar")
+    src = gz.make_source("lcg48", g["seed"])
+    chunks = []
+    for size in g["sizes"]:
+        buf = np.empty(size)
+        engine.fill_gaussians(smp, src, buf)
+        chunks.append(buf)
+    assert f64_to_hex(np.concatenate(chunks)) == g["out"]
+    assert spare_hex(smp) == g["spare"]
+
+
+def test_engine_and_per_call_interleave():
+    """tests/test_engine.py:43-55: batch then per-call continue one stream."""
+    smp, src = gz.make_sampler("ziggurat"), gz.make_source("splitmix", 7)
+    buf = np.empty(1000)
+    engine.fill_gaussians(smp, src, buf)
+    tail = [smp.next_gaussian(src) for _ in range(20)]
+    ref, *_ = O.fill_gaussians("ziggurat", "splitmix", np.array([[7, O.GOLDEN_GAMMA]], dtype=np.uint64), 1020)
+    assert bits_equal(np.concatenate([buf, tail]), ref[0])
+
+
+@pytest.mark.parametrize("source", ["lcg48", "splitmix"])
+def test_fill_u64_matches_reference(source, golden):
+    g = golden["u64"][source]
+    src = gz.make_source(source, g["seed"])
+    buf = np.empty(g["n"], dtype=np.uint64)
+    engine.fill_u64(src, buf)
+    assert sha(buf) == g["sha256"]
+    assert "%016x" % src.state == g["state"]
+
+
+def test_scripted_source_is_refused():
+    smp = gz.make_sampler("ziggurat")
+    assert not engine.supports(gz.ScriptedSource([1, 2, 3]))
+    assert engine.supports(gz.make_source("lcg48", 0)) and engine.supports(gz.make_source("splitmix", 0))
+    with pytest.raises(TypeError):
+        engine.fill_gaussians(smp, gz.ScriptedSource([1, 2, 3]), np.empty(4))
+
+
+# ---- multi-stream hot path ------------------------------------------------------
+
+@pytest.mark.parametrize("source,alg", PAIRINGS)
+@pytest.mark.parametrize("n_per", [1, 2, 7, 31, 32, 33, 63, 64, 65, 127, 128, 129, 255, 256, 257, 1000])
+def test_random_streams_vs_oracle(source, alg, n_per):
+    rng = np.random.default_rng(zlib.crc32(f"{source}/{alg}/{n_per}".encode()))
+    n = 2048 if n_per <= 257 else 512
+    raw = rng.integers(0, 2 ** 63, size=(n, 2), dtype=np.uint64) * np.uint64(2) + rng.integers(0, 2, size=(n, 2),
+                                                                                                   dtype=np.uint64)
+    if source == "lcg48":
+        st_np = raw[:, 0] & np.uint64((1 << 48) - 1)
+    else:
+        st_np = raw.copy()
+        st_np[:, 1] |= np.uint64(1)
+    st = dev_states(source, st_np)
+    out = torch.empty((n, n_per), dtype=torch.float64, device=DEV)
+    kw = {}
+    if alg == "polar":
+        has = rng.integers(0, 2, size=n).astype(np.uint8)
+        spare = rng.standard_normal(n) * has
+        kw = dict(spare=torch.from_numpy(spare).to(DEV), has_spare=torch.from_numpy(has).to(DEV))
+    streams.fill_gaussians_streams(alg, source, st, out, **kw)
+    ref, ref_st, ref_sp, ref_has, status = O.fill_gaussians(
+        alg, source, st_np, n_per, *( (spare, has) if alg == "polar" else (None, None)))
+    assert status == 0
+    got = out.cpu().numpy()
+    diff = np.nonzero((got.view(np.uint64) != ref.view(np.uint64)).any(axis=1))[0]
+    assert diff.size == 0, f"{diff.size} streams differ, first {diff[:5]}"
+    assert np.array_equal(u64(st), ref_st)
+    if alg == "polar":
+        assert np.array_equal(kw["has_spare"].cpu().numpy(), ref_has)
+        assert bits_equal(kw["spare"].cpu().numpy() * (ref_has > 0), ref_sp * (ref_has > 0))
+
+
+def test_strided_rows_and_fused_witnesses():
+    n, n_per, ld = 300, 200, 256
+    st_np = O.config_states("c4", range(n))
+    st = dev_states("lcg48", st_np)
+    big = torch.full((n, ld), -7.0, dtype=torch.float64, device=DEV)
+    out = big[:, :n_per]
+    ck = torch.zeros(n, dtype=torch.int64, device=DEV)
+    ps = torch.zeros((n, 4), dtype=torch.float64, device=DEV)
+    streams.fill_gaussians_streams("ziggurat", "lcg48", st, out, checksum=ck, psum=ps)
+    ref, *_ = O.fill_gaussians("ziggurat", "lcg48", st_np, n_per)
+    assert bits_equal(out.cpu().numpy(), ref)
+    assert (big[:, n_per:] == -7.0).all()
+    assert [("%016x" % v) for v in u64(ck)] == [xor_hex(ref[i]) for i in range(n)]
+    ps_ref = np.stack([ref.sum(1), (ref ** 2).sum(1), (ref ** 3).sum(1), (ref ** 4).sum(1)], 1)
+    np.testing.assert_allclose(ps.cpu().numpy(), ps_ref, rtol=1e-12, atol=1e-9)
+
+
+# ---- the five configs ---------------------------------------------------------
+
+def test_config1_full(golden):
+    g = golden["configs"]["c1"]
+    st = streams.config_states("c1", 0, 1024)
+    out = torch.empty((1024, 4096), dtype=torch.float64, device=DEV)
+    streams.fill_gaussians_streams("ziggurat", "splitmix", st, out)
+    got = out.cpu().numpy()
+    assert [xor_hex(got[i]) for i in range(1024)] == g["xor"]
+    assert ["%016x" % v for v in u64(st)[:, 0]] == g["state"]
+    assert sha(got) == g["sha256"]
+
+
+def _sampled(cfg, golden, n_total, n_per, alg, source):
+    recs = golden["configs"][cfg]
+    st = streams.config_states(cfg, 0, n_total)
+    out = torch.empty((n_total, n_per), dtype=torch.float64, device=DEV)
+    kw = {}
+    if alg == "polar":
+        kw = dict(spare=torch.zeros(n_total, dtype=torch.float64, device=DEV),
+                  has_spare=torch.zeros(n_total, dtype=torch.uint8, device=DEV))
+    ck = torch.zeros(n_total, dtype=torch.int64, device=DEV)
+    streams.fill_gaussians_streams(alg, source, st, out, checksum=ck, **kw)
+    ids = [r["id"] for r in recs if r["id"] < n_total]
+    rows = out[ids].cpu().numpy()
+    sts = u64(st)
+    cks = u64(ck)
+    for k, r in enumerate([r for r in recs if r["id"] < n_total]):
+        assert xor_hex(rows[k]) == r["xor"] and "%016x" % cks[r["id"]] == r["xor"]
+        assert f64_to_hex(rows[k, :4]) == r["first"]
+        assert "%016x" % int(sts.reshape(n_total, -1)[r["id"], 0]) == r["state"]
+    return out, st, ck
+
+
+def test_config2_full_size(golden):
+    out, st, ck = _sampled("c2", golden, 1 << 20, 256, "polar", "lcg48")
+    # every stream of a 64k-stream block against the oracle
+    ref, ref_st, *_ = O.fill_gaussians("polar", "lcg48", O.config_states("c2", range(65536)), 256)
+    assert bits_equal(out[:65536].cpu().numpy(), ref)
+    assert np.array_equal(u64(st)[:65536], ref_st)
+
+
+def test_config3_full_size(golden):
+    out, st, ck = _sampled("c3", golden, 1 << 20, 1024, "modified-ziggurat", "splitmix")
+    ids = np.random.default_rng(3).choice(1 << 20, 4096, replace=False)
+    ref, *_ = O.fill_gaussians("modified-ziggurat", "splitmix", O.config_states("c3", ids), 1024)
+    assert bits_equal(out[torch.from_numpy(ids).to(DEV)].cpu().numpy(), ref)
+
+
+def test_config4_shards_and_moments(golden):
+    """Config 4 on GPU 0's shard plus the sampled ids of other shards (seeded by
+    first_id), per-stream checksums and the global moments of a block."""
+    recs = golden["configs"]["c4"]
+    for r in recs:
+        st = streams.config_states("c4", r["id"], 1)
+        out = torch.empty((1, 256), dtype=torch.float64, device=DEV)
+        streams.fill_gaussians_streams("ziggurat", "lcg48", st, out)
+        assert xor_hex(out.cpu().numpy()[0]) == r["xor"]
+        assert "%016x" % int(u64(st)[0]) == r["state"]
+    g = golden["configs"]["c4_moments_first4096"]
+    st = streams.config_states("c4", 0, 4096)
+    out = torch.empty((4096, 256), dtype=torch.float64, device=DEV)
+    ps = torch.zeros((4096, 4), dtype=torch.float64, device=DEV)
+    ck = torch.zeros(4096, dtype=torch.int64, device=DEV)
+    streams.fill_gaussians_streams("ziggurat", "lcg48", st, out, psum=ps, checksum=ck)
+    assert sha(out.cpu().numpy()) == g["sha256"]
+    assert "%016x" % streams.xor_fold(ck) == g["xor_all"]
+    m = streams.moments_from_psum(ps, 256)
+    assert m.n == g["n"]
+    assert abs(m.mean - float.fromhex(g["mean"])) < 1e-12
+    assert abs(m.variance / float.fromhex(g["variance"]) - 1) < 1e-11
+    assert abs(m.skewness - float.fromhex(g["skewness"])) < 1e-9
+    assert abs(m.excess_kurtosis - float.fromhex(g["excess_kurtosis"])) < 1e-9
+
+
+def test_config5_mutation(golden):
+    n_ind, n_genes = 65536, 1024
+    x, sigma = streams.init_population(n_ind, n_genes, seed=2024, device=DEV)
+    st = streams.config_states("c5", 0, n_ind)
+    recs = golden["configs"]["c5"]
+    ids = [r["id"] for r in recs]
+    for r in recs:
+        assert sha(x[r["id"]].cpu().numpy()) == r["x0_sha256"]
+        assert float(sigma[r["id"]]) == float.fromhex(r["sigma"])
+    for gen in range(3):
+        streams.mutate(st, x, sigma, 1)
+        for r in recs:
+            gg = r["gens"][gen]
+            assert sha(x[r["id"]].cpu().numpy()) == gg["sha256"], (r["id"], gen)
+            assert "%016x" % int(u64(st)[r["id"], 0]) == gg["state"]
+    # the same three generations fused in one launch
+    x2, _ = streams.init_population(n_ind, n_genes, seed=2024, device=DEV)
+    st2 = streams.config_states("c5", 0, n_ind)
+    streams.mutate(st2, x2, sigma, 3)
+    assert torch.equal(x2, x) and torch.equal(st2, st)
+    del ids
+
+
+def test_mutate_short_rows_loop_generations():
+    n, genes = 100, 40  # rows shorter than a window: one launch per generation
+    st_np = O.config_states("c5", range(n))
+    x_np = np.random.default_rng(5).standard_normal((n, genes))
+    sig_np = np.abs(np.random.default_rng(6).standard_normal(n))
+    x = torch.from_numpy(x_np.copy()).to(DEV)
+    st = dev_states("splitmix", st_np)
+    streams.mutate(st, x, torch.from_numpy(sig_np).to(DEV), 4)
+    xr = x_np.copy()
+    ref_st, status = O.mutate(st_np, xr, sig_np, 4)
+    assert status == 0
+    assert bits_equal(x.cpu().numpy(), xr) and np.array_equal(u64(st), ref_st)
+
+
+# ---- guards, libm, misc ---------------------------------------------------------
+
+@pytest.mark.parametrize("alg,source,guard", [("polar", "lcg48", 1), ("polar", "splitmix", 2),
+                                              ("ziggurat", "splitmix", 1), ("ziggurat", "lcg48", 1),
+                                              ("modified-ziggurat", "splitmix", 1)])
+def test_guard_status_matches_oracle(alg, source, guard):
+    n, n_per = 4096, 64
+    cfg = "c2" if source == "lcg48" else "c3"
+    st_np = O.config_states(cfg, range(n))
+    *_, status = O.fill_gaussians(alg, source, st_np, n_per, guard=guard)
+    st = dev_states(source, st_np)
+    out = torch.empty((n, n_per), dtype=torch.float64, device=DEV)
+    if status == 1:
+        with pytest.raises(gz.RejectionLoopExceeded):
+            streams.fill_gaussians_streams(alg, source, st, out, guard=guard)
+    else:
+        streams.fill_gaussians_streams(alg, source, st, out, guard=guard)
+    # and with a guard that cannot trip, the same streams succeed
+    st = dev_states(source, st_np)
+    streams.fill_gaussians_streams(alg, source, st, out, guard=1000)
+
+
+def test_guard_exact_for_each_stream():
+    """Per stream, the device trips the guard exactly when the oracle does."""
+    n_per, guard = 16, 2
+    for sid in range(64):
+        st_np = O.config_states("c2", [sid])
+        *_, status = O.fill_gaussians("polar", "lcg48", st_np, n_per, guard=guard)
+        out = torch.empty((1, n_per), dtype=torch.float64, device=DEV)
+        try:
+            streams.fill_gaussians_streams("polar", "lcg48", dev_states("lcg48", st_np), out, guard=guard)
+            got = 0
+        except gz.RejectionLoopExceeded:
+            got = 1
+        assert got == status, sid
+
+
+@pytest.mark.parametrize("fn", [0, 1])
+def test_device_libm_bit_exact_sweep(fn):
+    """The kernels' exp/log restatement equals the host glibc bit for bit."""
+    import ctypes
+
+    from paper_2405_19493_b200 import _lib
+
+    L = _lib.load()
+    xs = O.sweep_inputs(fn, 1 << 24, 11 + fn)
+    d_in = torch.from_numpy(xs).to(DEV)
+    d_out = torch.empty_like(d_in)
+    s = torch.cuda.current_stream().cuda_stream
+    _lib.check(L.gz_libm_eval_device(fn, ctypes.c_void_p(d_in.data_ptr()), ctypes.c_void_p(d_out.data_ptr()),
+                                     xs.size, s))
+    bad, first = O.libm_mismatches(fn, xs, d_out.cpu().numpy())
+    assert bad == 0, f"{bad} mismatches, first input {xs[first]!r}"
+
+
+def test_unit_affine_and_seeding_match_oracle():
+    st = streams.config_states("c1", 5, 100)
+    assert np.array_equal(u64(st), O.config_states("c1", range(5, 105)))
+    st = streams.config_states("c2", 123, 50)
+    assert np.array_equal(u64(st), O.config_states("c2", range(123, 173)))
+    st = streams.config_states("c5", 7, 9)
+    assert np.array_equal(u64(st), O.config_states("c5", range(7, 16)))
+    x, sig = streams.init_population(4, 1024, seed=2024, first_ind=8191, total_ind=65536)
+    u, _ = O.fill_u64("splitmix", np.array([[(2024 + 8191 * 1024 * O.GOLDEN_GAMMA) & O.MASK64, O.GOLDEN_GAMMA]],
+                                           dtype=np.uint64), 4096)
+    ref = -5.0 + 10.0 * ((u[0] >> np.uint64(11)).astype(np.float64) * 2.0 ** -53)
+    assert bits_equal(x.reshape(-1).cpu().numpy(), ref)
+
+
+def test_zero_sizes():
+    st = streams.config_states("c2", 0, 8)
+    out = torch.empty((8, 0), dtype=torch.float64, device=DEV)
+    before = st.clone()
+    sp = torch.full((8,), 0.5, dtype=torch.float64, device=DEV)
+    hs = torch.ones(8, dtype=torch.uint8, device=DEV)
+    streams.fill_gaussians_streams("polar", "lcg48", st, out, spare=sp, has_spare=hs)
+    assert torch.equal(st, before) and (hs == 1).all() and (sp == 0.5).all()

@@ -1,0 +1,29 @@
+"""Quick device timing of each config's fill kernel (CUDA events, after warm-up)."""
+import sys, os, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+from paper_2405_19493_b200 import streams
+
+def t(cfg, n=None, reps=10):
+    c = streams.CONFIGS[cfg]
+    n = n or c.n_streams
+    st0 = streams.config_states(cfg, 0, n)
+    out = torch.empty((n, c.n_per), dtype=torch.float64, device="cuda")
+    kw = {}
+    if c.sampler == "polar":
+        kw = dict(spare=torch.zeros(n, dtype=torch.float64, device="cuda"), has_spare=torch.zeros(n, dtype=torch.uint8, device="cuda"))
+    for _ in range(3):
+        st = st0.clone(); streams.fill_gaussians_streams(c.sampler, c.source, st, out, sync=False, **kw)
+    torch.cuda.synchronize()
+    sts = [st0.clone() for _ in range(reps)]
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for k in range(reps):
+        streams.fill_gaussians_streams(c.sampler, c.source, sts[k], out, sync=False, **kw)
+    e1.record(); torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    nv = n * c.n_per
+    print(f"{cfg}: {n}x{c.n_per} {ms:.3f} ms  {nv/ms/1e6:.1f} Gvar/s  {nv*8/ms/1e6:.0f} GB/s", flush=True)
+
+for cfg in sys.argv[1:] or ["c1", "c2", "c3", "c4"]:
+    t(cfg)
