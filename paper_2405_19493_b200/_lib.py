@@ -19,7 +19,7 @@ SRC = {"lcg48": 0, "splitmix": 1}
 SEED = {"lcg_master_plus_id": 0, "sm_output_of_master": 1, "sm_id_xor_master": 2, "sm_master_plus_id": 3}
 DEFAULT_GUARD = 1_000_000
 
-EXPORTS = ("gz_version", "gz_last_error", "gz_device_count", "gz_set_device", "gz_tables_upload",
+EXPORTS = ("gz_version", "gz_last_error", "gz_device_count", "gz_set_kernel_policy", "gz_set_device", "gz_tables_upload",
            "gz_fill_gaussians", "gz_fill_gaussians_host", "gz_fill_u64", "gz_seed_streams",
            "gz_fill_unit_affine", "gz_mutate", "gz_moments_reduce", "gz_xor_reduce", "gz_stream_check",
            "gz_host_alloc", "gz_host_free", "gz_build_tables", "gz_libm_eval_device", "gz_libm_exp",
@@ -53,6 +53,7 @@ def load(require_device: bool = True):
             L.gz_last_error.restype = ctypes.c_char_p
             L.gz_device_count.restype = I
             L.gz_set_device.argtypes = [I]
+            L.gz_set_kernel_policy.argtypes = [I]
             L.gz_tables_upload.argtypes = [I, I, P, P, P, D]
             L.gz_fill_gaussians.argtypes = [I, I, I, i64, i64, i64, P, P, P, P, P, P, P, P, P, i64, P]
             L.gz_fill_gaussians_host.argtypes = [I, I, I, i64, i64, P, P, P, P, P, P, P, P, i64]

@@ -94,6 +94,12 @@ def fill_gaussians_streams(sampler, source, states, out, *, spare=None, has_spar
         check(L.gz_stream_check(s))
 
 
+def set_kernel_policy(policy: str) -> None:
+    """'auto', 'warp' (one warp decodes one stream) or 'lane' (one lane per stream)."""
+    L = _lib.load()
+    check(L.gz_set_kernel_policy({"auto": 0, "warp": 1, "lane": 2}[policy]))
+
+
 def fill_u64_streams(source, states, out, *, stream=None, sync: bool = True) -> None:
     """Raw draws: out[s, j] = j-th u64 of stream s (engine.py:224-232)."""
     L = _lib.load()

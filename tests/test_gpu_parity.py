@@ -132,11 +132,18 @@ def test_scripted_source_is_refused():
 
 # ---- multi-stream hot path ------------------------------------------------------
 
+@pytest.fixture(params=["warp", "lane"])
+def policy(request):
+    streams.set_kernel_policy(request.param)
+    yield request.param
+    streams.set_kernel_policy("auto")
+
+
 @pytest.mark.parametrize("source,alg", PAIRINGS)
-@pytest.mark.parametrize("n_per", [1, 2, 7, 31, 32, 33, 63, 64, 65, 127, 128, 129, 255, 256, 257, 1000])
-def test_random_streams_vs_oracle(source, alg, n_per):
+@pytest.mark.parametrize("n_per", [1, 2, 7, 15, 16, 17, 31, 32, 33, 63, 64, 65, 127, 128, 129, 255, 256, 257, 1000])
+def test_random_streams_vs_oracle(source, alg, n_per, policy):
     rng = np.random.default_rng(zlib.crc32(f"{source}/{alg}/{n_per}".encode()))
-    n = 2048 if n_per <= 257 else 512
+    n = 2011 if n_per <= 257 else 509     # not a multiple of 32: partial warps
     raw = rng.integers(0, 2 ** 63, size=(n, 2), dtype=np.uint64) * np.uint64(2) + rng.integers(0, 2, size=(n, 2),
                                                                                                    dtype=np.uint64)
     if source == "lcg48":
@@ -164,7 +171,7 @@ def test_random_streams_vs_oracle(source, alg, n_per):
         assert bits_equal(kw["spare"].cpu().numpy() * (ref_has > 0), ref_sp * (ref_has > 0))
 
 
-def test_strided_rows_and_fused_witnesses():
+def test_strided_rows_and_fused_witnesses(policy):
     n, n_per, ld = 300, 200, 256
     st_np = O.config_states("c4", range(n))
     st = dev_states("lcg48", st_np)
@@ -298,7 +305,7 @@ def test_mutate_short_rows_loop_generations():
 @pytest.mark.parametrize("alg,source,guard", [("polar", "lcg48", 1), ("polar", "splitmix", 2),
                                               ("ziggurat", "splitmix", 1), ("ziggurat", "lcg48", 1),
                                               ("modified-ziggurat", "splitmix", 1)])
-def test_guard_status_matches_oracle(alg, source, guard):
+def test_guard_status_matches_oracle(alg, source, guard, policy):
     n, n_per = 4096, 64
     cfg = "c2" if source == "lcg48" else "c3"
     st_np = O.config_states(cfg, range(n))
@@ -315,7 +322,7 @@ def test_guard_status_matches_oracle(alg, source, guard):
     streams.fill_gaussians_streams(alg, source, st, out, guard=1000)
 
 
-def test_guard_exact_for_each_stream():
+def test_guard_exact_for_each_stream(policy):
     """Per stream, the device trips the guard exactly when the oracle does."""
     n_per, guard = 16, 2
     for sid in range(64):
@@ -362,7 +369,7 @@ def test_unit_affine_and_seeding_match_oracle():
     assert bits_equal(x.reshape(-1).cpu().numpy(), ref)
 
 
-def test_zero_sizes():
+def test_zero_sizes(policy):
     st = streams.config_states("c2", 0, 8)
     out = torch.empty((8, 0), dtype=torch.float64, device=DEV)
     before = st.clone()

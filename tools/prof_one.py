@@ -1,0 +1,20 @@
+"""Run one config's fill a few times (for ncu captures): prof_one.py CFG [N_STREAMS] [REPS]."""
+import sys, os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+from paper_2405_19493_b200 import streams
+
+cfg = sys.argv[1]
+c = streams.CONFIGS[cfg]
+n = int(sys.argv[2]) if len(sys.argv) > 2 else c.n_streams
+reps = int(sys.argv[3]) if len(sys.argv) > 3 else 2
+st0 = streams.config_states(cfg, 0, n)
+out = torch.empty((n, c.n_per), dtype=torch.float64, device="cuda")
+kw = {}
+if c.sampler == "polar":
+    kw = dict(spare=torch.zeros(n, dtype=torch.float64, device="cuda"), has_spare=torch.zeros(n, dtype=torch.uint8, device="cuda"))
+for _ in range(reps):
+    st = st0.clone()
+    streams.fill_gaussians_streams(c.sampler, c.source, st, out, **kw)
+torch.cuda.synchronize()
+print("done", cfg, n)

@@ -25,5 +25,8 @@ def t(cfg, n=None, reps=10):
     nv = n * c.n_per
     print(f"{cfg}: {n}x{c.n_per} {ms:.3f} ms  {nv/ms/1e6:.1f} Gvar/s  {nv*8/ms/1e6:.0f} GB/s", flush=True)
 
+pol = os.environ.get("GZ_POLICY", "auto")
+streams.set_kernel_policy(pol)
+print("policy", pol)
 for cfg in sys.argv[1:] or ["c1", "c2", "c3", "c4"]:
     t(cfg)
