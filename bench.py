@@ -76,7 +76,7 @@ class ClockSampler:
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
@@ -286,7 +286,7 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-extra", action="store_true", help="skip the other four configs")
@@ -304,6 +304,7 @@ def main():
     # ---- headline: config 2 on every rank (weak scaling) ----
     first = rank * STREAMS_PER_GPU
     with ClockSampler(local) as clk:
+        time.sleep(0.3)   # let nvidia-smi start sampling before the timed region
         r = time_fill("c2", first, STREAMS_PER_GPU, args.steps, args.warmup, world)
     ms = allmax(r["ms_per_step"], world)
     value = world * r["variates_per_step"] / (ms / 1e3)
@@ -312,7 +313,7 @@ def main():
     achieved = kernel_bytes / (r["ms_per_step"] / 1e3) / 1e9
 
     # ---- e2e through the host-buffer C-ABI call ----
-    e = e2e_host(first, STREAMS_PER_GPU, max(2, args.steps // 3), 1)
+    e = e2e_host(first, STREAMS_PER_GPU, max(3, min(10, args.steps // 10)), 1)
     e_s = allmax(e["s_per_step"] * 1e3, world) / 1e3
     e2e = {"value": world * STREAMS_PER_GPU * N_PER / e_s, "unit": UNIT, "h2d_bytes_per_step": e["h2d"],
            "d2h_bytes_per_step": e["d2h"], "s_per_step": e_s}
@@ -321,14 +322,14 @@ def main():
     extra = {}
     launches = r["launches"]
     if not args.no_extra:
-        c1 = time_fill("c1", 0, 1024, max(20, args.steps), args.warmup, world)
+        c1 = time_fill("c1", 0, 1024, max(100, args.steps), args.warmup, world)
         extra["c1"] = {"value": world * c1["variates_per_step"] / (allmax(c1["ms_per_step"], world) / 1e3),
                        "ms_per_step": c1["ms_per_step"], "shape": "1024 x 4096 per GPU"}
         n3 = (1 << 20) // world
-        c3 = time_fill("c3", rank * n3, n3, args.steps, args.warmup, world)
+        c3 = time_fill("c3", rank * n3, n3, max(5, args.steps // 10), args.warmup, world)
         extra["c3"] = {"value": world * c3["variates_per_step"] / (allmax(c3["ms_per_step"], world) / 1e3),
                        "ms_per_step": c3["ms_per_step"], "shape": f"2^20 x 1024 box-wide, {n3} streams per GPU"}
-        c4 = time_fill("c4", rank * (1 << 22), 1 << 22, max(3, args.steps // 3), args.warmup, world, checks=True)
+        c4 = time_fill("c4", rank * (1 << 22), 1 << 22, max(5, args.steps // 10), args.warmup, world, checks=True)
         extra["c4"] = {"value": world * c4["variates_per_step"] / (allmax(c4["ms_per_step"], world) / 1e3),
                        "ms_per_step": c4["ms_per_step"], "shape": "2^22 x 256 per GPU, fused checksum + moments"}
         from paper_2405_19493_b200 import streams
@@ -336,15 +337,10 @@ def main():
         cen = streams.central_from_psum(c4["psum"], 256)
         xr = streams.xor_fold(c4["checksum"])
         if world > 1:
-            import torch.distributed as dist
+            from paper_2405_19493_b200 import dist as gzdist
 
-            parts = [torch.zeros(5, dtype=torch.float64, device="cuda") for _ in range(world)]
-            dist.all_gather(parts, cen)
-            xs = [torch.zeros(1, dtype=torch.int64, device="cuda") for _ in range(world)]
-            dist.all_gather(xs, torch.tensor([xr - (1 << 64) if xr >= (1 << 63) else xr], device="cuda"))
-            merged = streams.merge_central([tuple(p.cpu().tolist()) for p in parts])
-            for t in xs:
-                xr ^= int(t.item()) & ((1 << 64) - 1)
+            merged = gzdist.gather_moments(cen)
+            xr = gzdist.gather_xor(xr)
         else:
             merged = tuple(cen.cpu().tolist())
         m = streams.summarize(*merged)
@@ -352,7 +348,7 @@ def main():
         extra["c4"]["xor_all_streams"] = "%016x" % (xr & ((1 << 64) - 1))
         del c4
         n5 = 65536 // world
-        c5 = time_mutate(rank * n5, n5, 10, max(2, args.steps // 3), args.warmup, world)
+        c5 = time_mutate(rank * n5, n5, 10, max(3, args.steps // 20), args.warmup, world)
         extra["c5"] = {"value": world * c5["variates_per_step"] / (allmax(c5["ms_per_step"], world) / 1e3),
                        "ms_per_step": c5["ms_per_step"],
                        "shape": f"65536 x 1024 genes box-wide ({n5} per GPU), 10 generations per step"}
