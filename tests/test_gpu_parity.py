@@ -377,3 +377,19 @@ def test_zero_sizes(policy):
     hs = torch.ones(8, dtype=torch.uint8, device=DEV)
     streams.fill_gaussians_streams("polar", "lcg48", st, out, spare=sp, has_spare=hs)
     assert torch.equal(st, before) and (hs == 1).all() and (sp == 0.5).all()
+
+
+@pytest.mark.parametrize("layers", [8, 64, 512, 1024])
+@pytest.mark.parametrize("alg,source", [("ziggurat", "lcg48"), ("modified-ziggurat", "splitmix"),
+                                        ("ziggurat", "splitmix")])
+def test_custom_layer_counts(layers, alg, source, policy):
+    n, n_per = 777, 300
+    st_np = O.config_states("c4" if source == "lcg48" else "c3", range(1000, 1000 + n))
+    smp = gz.make_sampler(alg, layers=layers)
+    st = dev_states(source, st_np)
+    out = torch.empty((n, n_per), dtype=torch.float64, device=DEV)
+    streams.fill_gaussians_streams(smp, source, st, out)
+    ref, ref_st, *_ , status = O.fill_gaussians(alg, source, st_np, n_per, layers=layers)
+    assert status == 0
+    assert bits_equal(out.cpu().numpy(), ref)
+    assert np.array_equal(u64(st), ref_st)
