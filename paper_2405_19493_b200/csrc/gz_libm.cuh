@@ -48,10 +48,42 @@ GZ_HD uint64_t gz_host_bits(double d) { uint64_t u; memcpy(&u, &d, 8); return u;
 #define GZ_BITS(d) gz_host_bits(d)
 #endif
 
+/* Scalar coefficients: in the constant bank on the device (so DFMA takes them
+ * as c[][] operands instead of re-materialising 64-bit immediates), literal
+ * bit patterns on the host.  The 256-entry tables are passed by pointer (the
+ * kernels keep a shared-memory copy). */
+#if defined(__CUDACC__)
+static __constant__ double gzk_EXP_INVLN2N = GZ_EXP_INVLN2N_F;
+static __constant__ double gzk_EXP_SHIFT = GZ_EXP_SHIFT_F;
+static __constant__ double gzk_EXP_NEGLN2HIN = GZ_EXP_NEGLN2HIN_F;
+static __constant__ double gzk_EXP_NEGLN2LON = GZ_EXP_NEGLN2LON_F;
+static __constant__ double gzk_EXP_C2 = GZ_EXP_C2_F;
+static __constant__ double gzk_EXP_C3 = GZ_EXP_C3_F;
+static __constant__ double gzk_EXP_C4 = GZ_EXP_C4_F;
+static __constant__ double gzk_EXP_C5 = GZ_EXP_C5_F;
+static __constant__ double gzk_LOG_LN2HI = GZ_LOG_LN2HI_F;
+static __constant__ double gzk_LOG_LN2LO = GZ_LOG_LN2LO_F;
+static __constant__ double gzk_LOG_A0 = GZ_LOG_A0_F;
+static __constant__ double gzk_LOG_A1 = GZ_LOG_A1_F;
+static __constant__ double gzk_LOG_A2 = GZ_LOG_A2_F;
+static __constant__ double gzk_LOG_A3 = GZ_LOG_A3_F;
+static __constant__ double gzk_LOG_A4 = GZ_LOG_A4_F;
+static __constant__ double gzk_LOG_B0 = GZ_LOG_B0_F;
+static __constant__ double gzk_LOG_B1 = GZ_LOG_B1_F;
+static __constant__ double gzk_LOG_B2 = GZ_LOG_B2_F;
+static __constant__ double gzk_LOG_B3 = GZ_LOG_B3_F;
+static __constant__ double gzk_LOG_B4 = GZ_LOG_B4_F;
+static __constant__ double gzk_LOG_B5 = GZ_LOG_B5_F;
+static __constant__ double gzk_LOG_B6 = GZ_LOG_B6_F;
+static __constant__ double gzk_LOG_B7 = GZ_LOG_B7_F;
+static __constant__ double gzk_LOG_B8 = GZ_LOG_B8_F;
+static __constant__ double gzk_LOG_B9 = GZ_LOG_B9_F;
+static __constant__ double gzk_LOG_B10 = GZ_LOG_B10_F;
+#endif
 #if defined(__CUDA_ARCH__)
-/* Tables live in __constant__ for the rare scalar use and are copied into
- * shared memory by kernels that call these functions in bulk (see
- * gz_kernels.cu); the functions take the table pointer explicitly. */
+#define GZ_K(name) (gzk_##name)
+#else
+#define GZ_K(name) GZ_DBL(GZ_##name)
 #endif
 
 static const uint64_t gz_exp_tab_host[256] = GZ_EXP_TAB_INIT;
@@ -73,19 +105,19 @@ GZ_HD double gz_exp_t(double x, const uint64_t* __restrict__ tab)
         }
         special = 1;                               /* 512 <= |x| < 1024 */
     }
-    double kd = GZ_FMA(x, GZ_DBL(GZ_EXP_INVLN2N), GZ_DBL(GZ_EXP_SHIFT));
+    double kd = GZ_FMA(x, GZ_K(EXP_INVLN2N), GZ_K(EXP_SHIFT));
     uint64_t ki = GZ_BITS(kd);
-    kd = GZ_SUB(kd, GZ_DBL(GZ_EXP_SHIFT));
-    double r = GZ_FMA(kd, GZ_DBL(GZ_EXP_NEGLN2HIN), x);
-    r = GZ_FMA(kd, GZ_DBL(GZ_EXP_NEGLN2LON), r);
+    kd = GZ_SUB(kd, GZ_K(EXP_SHIFT));
+    double r = GZ_FMA(kd, GZ_K(EXP_NEGLN2HIN), x);
+    r = GZ_FMA(kd, GZ_K(EXP_NEGLN2LON), r);
     uint32_t idx = 2u * (uint32_t)(ki & 127u);
     uint64_t top = ki << 45;
     double tail = GZ_DBL(tab[idx]);
     uint64_t sbits = tab[idx + 1] + top;
-    double p23 = GZ_FMA(r, GZ_DBL(GZ_EXP_C3), GZ_DBL(GZ_EXP_C2));
+    double p23 = GZ_FMA(r, GZ_K(EXP_C3), GZ_K(EXP_C2));
     double tr = GZ_ADD(r, tail);
     double r2 = GZ_MUL(r, r);
-    double p45 = GZ_FMA(r, GZ_DBL(GZ_EXP_C5), GZ_DBL(GZ_EXP_C4));
+    double p45 = GZ_FMA(r, GZ_K(EXP_C5), GZ_K(EXP_C4));
     double t = GZ_FMA(p23, r2, tr);
     double r4 = GZ_MUL(r2, r2);
     double tmp = GZ_FMA(r4, p45, t);
@@ -124,20 +156,20 @@ GZ_HD double gz_log_t(double x, const uint64_t* __restrict__ tab)
         double r = GZ_SUB(x, 1.0);
         double r2 = GZ_MUL(r, r);
         double r3 = GZ_MUL(r, r2);
-        double p1 = GZ_FMA(r2, GZ_DBL(GZ_LOG_B3), GZ_FMA(r, GZ_DBL(GZ_LOG_B2), GZ_DBL(GZ_LOG_B1)));
-        double p2 = GZ_FMA(r2, GZ_DBL(GZ_LOG_B6), GZ_FMA(r, GZ_DBL(GZ_LOG_B5), GZ_DBL(GZ_LOG_B4)));
-        double p3 = GZ_FMA(r3, GZ_DBL(GZ_LOG_B10),
-                           GZ_FMA(r2, GZ_DBL(GZ_LOG_B9), GZ_FMA(r, GZ_DBL(GZ_LOG_B8), GZ_DBL(GZ_LOG_B7))));
+        double p1 = GZ_FMA(r2, GZ_K(LOG_B3), GZ_FMA(r, GZ_K(LOG_B2), GZ_K(LOG_B1)));
+        double p2 = GZ_FMA(r2, GZ_K(LOG_B6), GZ_FMA(r, GZ_K(LOG_B5), GZ_K(LOG_B4)));
+        double p3 = GZ_FMA(r3, GZ_K(LOG_B10),
+                           GZ_FMA(r2, GZ_K(LOG_B9), GZ_FMA(r, GZ_K(LOG_B8), GZ_K(LOG_B7))));
         double q = GZ_FMA(p3, r3, p2);
         q = GZ_FMA(q, r3, p1);
         double t = GZ_FMA(r, 134217728.0, r);          /* r + r*2^27 */
         double rhi = GZ_FMA(-134217728.0, r, t);       /* t - r*2^27 */
         double rhi2 = GZ_MUL(rhi, rhi);
         double rlo = GZ_SUB(r, rhi);
-        double hi = GZ_FMA(rhi2, GZ_DBL(GZ_LOG_B0), r);
-        double lo = GZ_FMA(rhi2, GZ_DBL(GZ_LOG_B0), GZ_SUB(r, hi));
+        double hi = GZ_FMA(rhi2, GZ_K(LOG_B0), r);
+        double lo = GZ_FMA(rhi2, GZ_K(LOG_B0), GZ_SUB(r, hi));
         double rr = GZ_ADD(r, rhi);
-        double c = GZ_MUL(GZ_DBL(GZ_LOG_B0), rlo);
+        double c = GZ_MUL(GZ_K(LOG_B0), rlo);
         lo = GZ_FMA(c, rr, lo);
         double y = GZ_FMA(q, r3, lo);
         return GZ_ADD(hi, y);
@@ -159,16 +191,16 @@ GZ_HD double gz_log_t(double x, const uint64_t* __restrict__ tab)
     double logc = GZ_DBL(tab[2 * i + 1]);
     double z = GZ_DBL(iz);
     double kd = (double)k;
-    double w = GZ_FMA(kd, GZ_DBL(GZ_LOG_LN2HI), logc);
+    double w = GZ_FMA(kd, GZ_K(LOG_LN2HI), logc);
     double r = GZ_FMA(z, invc, -1.0);
-    double a12 = GZ_FMA(r, GZ_DBL(GZ_LOG_A2), GZ_DBL(GZ_LOG_A1));
+    double a12 = GZ_FMA(r, GZ_K(LOG_A2), GZ_K(LOG_A1));
     double hi = GZ_ADD(r, w);
     double r2 = GZ_MUL(r, r);
     double lo = GZ_ADD(GZ_SUB(w, hi), r);
-    lo = GZ_FMA(kd, GZ_DBL(GZ_LOG_LN2LO), lo);
+    lo = GZ_FMA(kd, GZ_K(LOG_LN2LO), lo);
     double r3 = GZ_MUL(r, r2);
-    double a34 = GZ_FMA(r, GZ_DBL(GZ_LOG_A4), GZ_DBL(GZ_LOG_A3));
-    double t = GZ_FMA(r2, GZ_DBL(GZ_LOG_A0), lo);
+    double a34 = GZ_FMA(r, GZ_K(LOG_A4), GZ_K(LOG_A3));
+    double t = GZ_FMA(r2, GZ_K(LOG_A0), lo);
     double a = GZ_FMA(a34, r2, a12);
     double y = GZ_FMA(r3, a, t);
     return GZ_ADD(y, hi);

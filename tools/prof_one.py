@@ -4,6 +4,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2405_19493_b200 import streams
 
+streams.set_kernel_policy(os.environ.get("GZ_POLICY", "auto"))
 cfg = sys.argv[1]
 c = streams.CONFIGS[cfg]
 n = int(sys.argv[2]) if len(sys.argv) > 2 else c.n_streams
