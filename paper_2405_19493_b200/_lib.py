@@ -11,7 +11,7 @@ import os
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libgzb200.so")
+LIB_PATH = os.environ.get("GZ_LIB") or os.path.join(HERE, "libgzb200.so")   # GZ_LIB: alternate build (experiments)
 
 GZ_OK, GZ_ERR_GUARD, GZ_ERR_INVALID, GZ_ERR_CUDA = 0, 1, 2, 3
 ALG = {"polar": 0, "ziggurat": 1, "modified-ziggurat": 2}
