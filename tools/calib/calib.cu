@@ -7,42 +7,42 @@
 
 constexpr int WARPS = 8;
 
-template <int LK, int LSTRIDE>
-__device__ __forceinline__ void flushK(const double* ring, double* out, int64_t ld, int64_t row0, int f, int lane) {
-    constexpr int LRING = 2 * LK;
+template <int LK, int LSTRIDE, int LRING>
+__device__ __forceinline__ void flushK(const double* ring, double* out, int64_t ld, int64_t row0, int f, int c0, int lane) {
     constexpr int LPR = LK / 2;            // lanes per row (16 B each)
     constexpr int RPI = 32 / LPR;          // rows per instruction
-    const int c0 = f & (LRING - 1);
     const int q = lane % LPR, rq = lane / LPR;
     double* base = out + (row0 + rq) * ld + f + 2 * q;
-    const double* src = ring + rq * LSTRIDE + c0 + 2 * q;
+    int ca = c0 + 2 * q; if (ca >= LRING) ca -= LRING;
+    int cb = ca + 1; if (cb >= LRING) cb -= LRING;
+    const double* src = ring + rq * LSTRIDE;
 #pragma unroll
     for (int it = 0; it < 32 / RPI; ++it)
-        *reinterpret_cast<double2*>(base + (int64_t)(it * RPI) * ld) = make_double2(src[it * RPI * LSTRIDE], src[it * RPI * LSTRIDE + 1]);
+        *reinterpret_cast<double2*>(base + (int64_t)(it * RPI) * ld) = make_double2(src[it * RPI * LSTRIDE + ca], src[it * RPI * LSTRIDE + cb]);
 }
 
 // MODE 0: staging only (value = w); 1: + LCG draw -> double; 2: + table lookup/compare (always accept);
 // 3: direct (uncoalesced) stores instead of staging, with LCG draw
-template <int MODE, int LK, int OCC>
-__global__ void __launch_bounds__(256, OCC) k(int64_t n_streams, int n_per, const uint64_t* st_in, double* out, const ulonglong2* kwg) {
+template <int MODE, int LK, int LRING, int NW, int OCC>
+__global__ void __launch_bounds__(NW * 32, OCC) k(int64_t n_streams, int n_per, const uint64_t* st_in, double* out, const ulonglong2* kwg) {
     extern __shared__ __align__(16) unsigned char smem[];
     ulonglong2* s_kw = reinterpret_cast<ulonglong2*>(smem);
     double* s_ring = reinterpret_cast<double*>(smem + 16 * 128);
     for (int i = threadIdx.x; i < 128; i += blockDim.x) s_kw[i] = kwg[i];
     __syncthreads();
-    constexpr int LRING = 2 * LK, LSTRIDE = LRING + 1;
+    constexpr int LSTRIDE = LRING + 1;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     double* ring = s_ring + wib * 32 * LSTRIDE;
     double* myring = ring + lane * LSTRIDE;
     const int64_t n_groups = (n_streams + 31) >> 5;
-    for (int64_t grp = (int64_t)blockIdx.x * WARPS + wib; grp < n_groups; grp += (int64_t)gridDim.x * WARPS) {
+    for (int64_t grp = (int64_t)blockIdx.x * NW + wib; grp < n_groups; grp += (int64_t)gridDim.x * NW) {
         const int64_t row0 = grp * 32, sid = row0 + lane;
         uint64_t S = st_in[sid];
-        int w = 0, flushed = 0;
+        int w = 0, flushed = 0, wslot = 0, fslot = 0;
         while (flushed < n_per) {
             const int lim = min(n_per, flushed + LRING);
 #pragma unroll 2
-            for (int it = 0; it < LK; ++it) {
+            for (int it = 0; it < LK; ++it) {   // (wrap of the ring row handled by the flush reading contiguous LK)
                 if (w < lim) {
                     double v;
                     if constexpr (MODE == 0) {
@@ -63,13 +63,15 @@ __global__ void __launch_bounds__(256, OCC) k(int64_t n_streams, int n_per, cons
                         }
                     }
                     if constexpr (MODE == 3) out[sid * (int64_t)n_per + w] = v;
-                    else myring[w & (LRING - 1)] = v;
+                    else myring[wslot] = v;
                     ++w;
+                    wslot = (wslot + 1 == LRING) ? 0 : wslot + 1;
                 }
             }
             if constexpr (MODE != 3) {
                 __syncwarp();
-                flushK<LK, LSTRIDE>(ring, out, n_per, row0, flushed, lane);
+                flushK<LK, LSTRIDE, LRING>(ring, out, n_per, row0, flushed, fslot, lane);
+                fslot = (fslot + LK >= LRING) ? fslot + LK - LRING : fslot + LK;
                 __syncwarp();
             }
             flushed += LK;
@@ -92,25 +94,30 @@ int main() {
     cudaMalloc(&kw, 128 * 16); cudaMemset(kw, 0x7f, 128 * 16);
     cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
     int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    auto run = [&](auto kern, const char* name, int lk) {
-        const size_t smem = 16 * 128 + WARPS * 32 * (2 * lk + 1) * 8;
+    auto run = [&](auto kern, const char* name, int lring, int nw) {
+        const size_t smem = 16 * 128 + nw * 32 * (lring + 1) * 8;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        int occ; cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem);
+        int occ;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, nw * 32, smem);
         int grid = sms * occ;
-        for (int r = 0; r < 2; ++r) kern<<<grid, 256, smem>>>(n_streams, n_per, st, out, kw);
+        for (int r = 0; r < 2; ++r) kern<<<grid, nw * 32, smem>>>(n_streams, n_per, st, out, kw);
         cudaEventRecord(a);
-        for (int r = 0; r < 5; ++r) kern<<<grid, 256, smem>>>(n_streams, n_per, st, out, kw);
+        for (int r = 0; r < 5; ++r) kern<<<grid, nw * 32, smem>>>(n_streams, n_per, st, out, kw);
         cudaEventRecord(b); cudaEventSynchronize(b);
         float ms; cudaEventElapsedTime(&ms, a, b); ms /= 5;
         printf("%-28s occ=%d  %.3f ms  %.1f Gvar/s  %.0f GB/s  err=%s\n", name, occ, ms, n_streams * n_per / ms / 1e6,
                n_streams * n_per * 8 / ms / 1e6, cudaGetErrorString(cudaGetLastError()));
     };
-    run(k<0, 8, 6>, "staging only LK=8", 8);
-    run(k<0, 16, 3>, "staging only LK=16", 16);
-    run(k<0, 32, 1>, "staging only LK=32", 32);
-    run(k<2, 8, 6>, "lcg+table+staging LK=8", 8);
-    run(k<2, 16, 3>, "lcg+table+staging LK=16", 16);
-    run(k<2, 32, 1>, "lcg+table+staging LK=32", 32);
+    run(k<0, 16, 32, 8, 1>, "stage LK16 R32 8w", 32, 8);
+    run(k<2, 16, 32, 8, 1>, "lcg  LK16 R32 8w", 32, 8);
+    run(k<0, 32, 40, 6, 1>, "stage LK32 R40 6w", 40, 6);
+    run(k<2, 32, 40, 6, 1>, "lcg  LK32 R40 6w", 40, 6);
+    run(k<0, 32, 48, 4, 1>, "stage LK32 R48 4w", 48, 4);
+    run(k<2, 32, 48, 4, 1>, "lcg  LK32 R48 4w", 48, 4);
+    run(k<0, 32, 64, 4, 1>, "stage LK32 R64 4w", 64, 4);
+    run(k<2, 32, 64, 4, 1>, "lcg  LK32 R64 4w", 64, 4);
+    run(k<0, 64, 72, 2, 1>, "stage LK64 R72 2w", 72, 2);
+    run(k<2, 64, 72, 2, 1>, "lcg  LK64 R72 2w", 72, 2);
     {
         int grid = sms * 8;
         k_store<<<grid, 256>>>(n_streams * n_per, out);
