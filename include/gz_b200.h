@@ -165,6 +165,20 @@ int gz_xor_reduce(const uint64_t* in, int64_t n, uint64_t* out, void* cuda_strea
  */
 int gz_stream_check(void* cuda_stream);
 
+/*
+ * On-device verification statistics (device pointers):
+ *   gz_hist_edges   counts[k] = #{x : number of edges <= x == k}, k = 0..n_edges
+ *                   (numpy.searchsorted(edges, x, side="right"); edges sorted;
+ *                   stats.py:276-315 chi_square_gof binning); n_edges < 4096
+ *   gz_ks_stat      d_out = {D+, D-} of the sample against 0.5*erfc(-x/sqrt 2)
+ *                   (stats.py:262-273); n < 2^31
+ *   gz_lowbits_hist counts[c] = #{x : (x & (2^k - 1)) == c}, 1 <= k <= 8
+ *                   (stats.py:334-353 low_bits_chi_square)
+ */
+int gz_hist_edges(const double* x, int64_t n, const double* edges, int n_edges, uint64_t* counts, void* cuda_stream);
+int gz_ks_stat(const double* x, int64_t n, double* d_out, void* cuda_stream);
+int gz_lowbits_hist(const uint64_t* x, int64_t n, int k_bits, uint64_t* counts, void* cuda_stream);
+
 /* Pinned host memory helpers (for gz_fill_gaussians_host at full PCIe speed). */
 int gz_host_alloc(void** ptr, int64_t bytes);
 int gz_host_free(void* ptr);

@@ -234,6 +234,23 @@ def main():
     cfg["c5"] = recs
     g["configs"] = cfg
 
+    # statistical gates (stats.py) on a known deviate buffer
+    from gausszig import stats as S
+    st = {"edges10": [v.hex() for v in S.equal_probability_edges(10)],
+          "edges100": [v.hex() for v in S.equal_probability_edges(100)],
+          "normal_cdf": {repr(x): S.normal_cdf(x).hex() for x in (-3.0, -0.5, 0.0, 1.7)},
+          "chi_square_sf": [[x, k, S.chi_square_sf(x, k).hex()] for x, k in
+                            ((3.0, 4), (50.0, 40), (120.5, 99), (0.5, 1), (250.0, 199), (30.0, 7))]}
+    buf, _ = fill("ziggurat", make_source("lcg48", 424242), 300_000)
+    gr = S.chi_square_gof(buf, S.equal_probability_edges(100))
+    kr = S.ks_test(buf)
+    st["gof_zig_lcg_424242"] = {"statistic": gr.statistic.hex(), "dof": gr.dof, "p_value": gr.p_value.hex(),
+                                "ks_d": kr.d_statistic.hex(), "n": kr.n}
+    for sid in ("lcg48", "splitmix"):
+        r = S.low_bits_chi_square(make_source(sid, 5), 4, 100_000)
+        st["lowbits_" + sid] = {"seed": 5, "k": 4, "n": 100_000, "statistic": r.statistic.hex(), "dof": r.dof}
+    g["stats"] = st
+
     with open(OUT, "w") as f:
         json.dump(g, f, indent=0, sort_keys=True)
     print("wrote", OUT, os.path.getsize(OUT), "bytes")

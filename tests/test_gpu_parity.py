@@ -393,3 +393,34 @@ def test_custom_layer_counts(layers, alg, source, policy):
     assert status == 0
     assert bits_equal(out.cpu().numpy(), ref)
     assert np.array_equal(u64(st), ref_st)
+
+
+# ---- on-device verification statistics ---------------------
+
+def test_device_chi_square_and_ks_match_reference(golden):
+    from paper_2405_19493_b200 import verify as V
+
+    g = golden["stats"]["gof_zig_lcg_424242"]
+    out = torch.empty(300_000, dtype=torch.float64, device=DEV)
+    engine.fill_gaussians(gz.make_sampler("ziggurat"), gz.make_source("lcg48", 424242), out)
+    edges = V.equal_probability_edges(100)
+    counts = V.histogram(out, edges)
+    ref_counts = np.bincount(np.searchsorted(np.array(edges), out.cpu().numpy(), side="right"), minlength=101)
+    assert np.array_equal(counts, ref_counts)
+    r = V.chi_square_gof(out, edges)
+    assert r.dof == g["dof"]
+    assert r.statistic == pytest.approx(float.fromhex(g["statistic"]), rel=1e-12)
+    assert r.p_value == pytest.approx(float.fromhex(g["p_value"]), rel=1e-9)
+    k = V.ks_test(out)
+    assert k.n == g["n"]
+    assert k.d_statistic == pytest.approx(float.fromhex(g["ks_d"]), abs=1e-14)
+
+
+@pytest.mark.parametrize("source", ["lcg48", "splitmix"])
+def test_device_low_bits_chi_square_matches_reference(source, golden):
+    from paper_2405_19493_b200 import verify as V
+
+    g = golden["stats"]["lowbits_" + source]
+    r = V.low_bits_chi_square(gz.make_source(source, g["seed"]), g["k"], g["n"])
+    assert r.dof == g["dof"]
+    assert r.statistic == pytest.approx(float.fromhex(g["statistic"]), rel=1e-12)
