@@ -251,6 +251,16 @@ def main():
         st["lowbits_" + sid] = {"seed": 5, "k": 4, "n": 100_000, "statistic": r.statistic.hex(), "dof": r.dof}
     g["stats"] = st
 
+    # bench checksum witness (bench.py:209-216): xor fold of WITNESS_OPS deviates of one fresh stream
+    from gausszig import bench as B
+    wit = {}
+    for seed in (0x5EEDBA5E, 60):
+        for sid in ("lcg48", "splitmix"):
+            for alg in ("polar", "ziggurat", "modified-ziggurat"):
+                buf, _ = fill(alg, make_source(sid, seed), B.WITNESS_OPS)
+                wit["%s/%s/%d" % (sid, alg, seed)] = "%016x" % B._checksum_fold(buf)
+    g["bench_witness"] = wit
+
     with open(OUT, "w") as f:
         json.dump(g, f, indent=0, sort_keys=True)
     print("wrote", OUT, os.path.getsize(OUT), "bytes")

@@ -424,3 +424,25 @@ def test_device_low_bits_chi_square_matches_reference(source, golden):
     r = V.low_bits_chi_square(gz.make_source(source, g["seed"]), g["k"], g["n"])
     assert r.dof == g["dof"]
     assert r.statistic == pytest.approx(float.fromhex(g["statistic"]), rel=1e-12)
+
+
+# ---- benchmark harness with the reference's schema -------------
+
+@pytest.mark.parametrize("source,alg", [p for p in PAIRINGS if p != ("lcg48", "modified-ziggurat")])
+def test_benchmark_witness_equals_reference_checksum(source, alg, golden):
+    from paper_2405_19493_b200 import benchmark as B
+
+    cfg = B.BenchConfig.smoke(seed=60)
+    r = B.run_benchmark(alg, source, cfg)
+    assert "%016x" % r.checksum == golden["bench_witness"]["%s/%s/60" % (source, alg)]
+    assert r.ns_per_op > 0 and len(r.per_iteration_ns_per_op) == cfg.measure_iters
+    assert r.engine_used == "cuda"
+    text = B.render_table([r], "md")
+    assert text.startswith("| PRNG |") and source in text
+
+
+def test_benchmark_refuses_unsanctioned_pairing():
+    from paper_2405_19493_b200 import benchmark as B
+
+    with pytest.raises(gz.UnsanctionedPairing):
+        B.run_benchmark("modified-ziggurat", "lcg48", B.BenchConfig.smoke())
