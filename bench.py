@@ -53,10 +53,12 @@ def peaks():
 
 
 def traffic_record(cfg):
-    """dram bytes per launch of the headline kernel from the committed ncu capture."""
+    """dram read + write bytes per launch of the headline kernel, from the committed
+    `ncu --set full` capture (profiles/traffic.json), or None."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            return json.load(f).get(cfg)
+            rec = json.load(f).get(cfg)
+        return None if rec is None else rec["bytes_per_launch"]
     except Exception:
         return None
 
