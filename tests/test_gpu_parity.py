@@ -286,6 +286,26 @@ def test_config5_mutation(golden):
     del ids
 
 
+@pytest.mark.parametrize("n,genes,gens,pad", [(100, 32, 3, 0), (2011, 48, 2, 0), (700, 64, 5, 2), (333, 1024, 2, 0),
+                                              (97, 96, 3, 1), (64, 40, 2, 0), (40, 16, 4, 0)])
+def test_mutate_vs_oracle(n, genes, gens, pad, policy):
+    """gz_mutate on both kernel families: rows of any length, strided (pad) and
+    8-byte-aligned-only (odd ld) rows, several generations per launch."""
+    st_np = O.config_states("c5", range(n))
+    x_np = np.random.default_rng(genes).standard_normal((n, genes))
+    sig_np = np.abs(np.random.default_rng(n).standard_normal(n))
+    full = torch.zeros((n, genes + pad), dtype=torch.float64, device=DEV)
+    full[:, :genes] = torch.from_numpy(x_np)
+    x = full[:, :genes]
+    st = dev_states("splitmix", st_np)
+    streams.mutate(st, x, torch.from_numpy(sig_np).to(DEV), gens)
+    xr = x_np.copy()
+    ref_st, status = O.mutate(st_np, xr, sig_np, gens)
+    assert status == 0
+    assert bits_equal(x.cpu().numpy(), xr) and np.array_equal(u64(st), ref_st)
+    assert (full[:, genes:] == 0).all()
+
+
 def test_mutate_short_rows_loop_generations():
     n, genes = 100, 40  # rows shorter than a window: one launch per generation
     st_np = O.config_states("c5", range(n))

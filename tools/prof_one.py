@@ -6,6 +6,14 @@ from paper_2405_19493_b200 import streams
 
 streams.set_kernel_policy(os.environ.get("GZ_POLICY", "auto"))
 cfg = sys.argv[1]
+if cfg == "c5":
+    x, sig = streams.init_population(65536, 1024, seed=2024)
+    st = streams.config_states("c5", 0, 65536)
+    for _ in range(int(sys.argv[3]) if len(sys.argv) > 3 else 2):
+        streams.mutate(st, x, sig, 10)
+    torch.cuda.synchronize()
+    print("done c5")
+    raise SystemExit(0)
 c = streams.CONFIGS[cfg]
 n = int(sys.argv[2]) if len(sys.argv) > 2 else c.n_streams
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 2

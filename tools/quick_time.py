@@ -4,7 +4,26 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2405_19493_b200 import streams
 
+def t5(reps=5, gens=10):
+    n, genes = 65536, 1024
+    x, sig = streams.init_population(n, genes, seed=2024)
+    st = streams.config_states("c5", 0, n)
+    for _ in range(2):
+        streams.mutate(st, x, sig, gens, sync=False)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        streams.mutate(st, x, sig, gens, sync=False)
+    e1.record(); torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    nv = n * genes * gens
+    print(f"c5: {n}x{genes}x{gens} {ms:.3f} ms  {nv/ms/1e6:.1f} Gvar/s  {nv*16/ms/1e6:.0f} GB/s", flush=True)
+
+
 def t(cfg, n=None, reps=10):
+    if cfg == "c5":
+        return t5()
     c = streams.CONFIGS[cfg]
     n = n or c.n_streams
     st0 = streams.config_states(cfg, 0, n)
