@@ -146,6 +146,8 @@ GZ_HD double gz_exp_t(double x, const uint64_t* __restrict__ tab)
     return GZ_MUL(y, GZ_DBL(0x0010000000000000ULL) /* 0x1p-1022 */);
 }
 
+GZ_HD double gz_log_core(uint64_t ix, const uint64_t* __restrict__ tab);
+
 /* log(x): glibc's log (FMA variant).  `tab` is the 256-entry GZ_LOG_TAB. */
 GZ_HD double gz_log_t(double x, const uint64_t* __restrict__ tab)
 {
@@ -183,6 +185,14 @@ GZ_HD double gz_log_t(double x, const uint64_t* __restrict__ tab)
         /* subnormal: normalise */
         ix = GZ_BITS(GZ_MUL(x, 4503599627370496.0 /* 2^52 */)) - (52ULL << 52);
     }
+    return gz_log_core(ix, tab);
+}
+
+/* glibc log's table path for the bit pattern of a positive normal x outside the
+   near-1 interval (the tail of gz_log_t, callable directly when the caller
+   already knows the branch) */
+GZ_HD double gz_log_core(uint64_t ix, const uint64_t* __restrict__ tab)
+{
     uint64_t tmp = ix - 0x3fe6000000000000ULL;
     uint32_t i = (uint32_t)(tmp >> 45) & 127u;
     int32_t k = (int32_t)((int64_t)tmp >> 52);

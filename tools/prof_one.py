@@ -15,7 +15,7 @@ if cfg == "c5":
     print("done c5")
     raise SystemExit(0)
 c = streams.CONFIGS[cfg]
-n = int(sys.argv[2]) if len(sys.argv) > 2 else c.n_streams
+n = int(sys.argv[2]) if len(sys.argv) > 2 and int(sys.argv[2]) > 0 else c.n_streams
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 2
 st0 = streams.config_states(cfg, 0, n)
 out = torch.empty((n, c.n_per), dtype=torch.float64, device="cuda")
