@@ -156,6 +156,24 @@ int gz_mutate(int table_slot, int64_t n_ind, int64_t n_genes, int64_t ld, const 
 int gz_moments_reduce(const double* psum, int64_t n_rows, int64_t values_per_row, double* out5,
                       void* cuda_stream);
 
+/*
+ * out5 = {n, mean, M2, M3, M4} of a raw f64 buffer x[n] (device pointers), by
+ * fixed-order block power sums: the moments of stats.py:232-259 for the
+ * `verify` command (cli.py:160-175) over deviates already in HBM.
+ */
+int gz_moments_buffer(const double* x, int64_t n, double* out5, void* cuda_stream);
+
+/*
+ * Layer occupancy of one ziggurat stream (samplers.py:89-93 / 138-142
+ * sample_with_occupancy, used by cli.py:185-192): n_calls sequential calls,
+ * counts[i] (device u64[n_layers]) = attempts that selected layer i, out
+ * (device f64[n_calls], may be NULL) = the deviates, state advanced
+ * (state_in/state_out device, 1 or 2 words).  Single-threaded on the device;
+ * meant for <= 1e6 calls.  Guard trips are reported by gz_stream_check.
+ */
+int gz_zig_occupancy(int alg, int src, int table_slot, const uint64_t* state_in, uint64_t* state_out,
+                     int64_t n_calls, double* out, uint64_t* counts, int64_t guard, void* cuda_stream);
+
 /* xor-fold of u64[n] (device) into *out (device): the global checksum. */
 int gz_xor_reduce(const uint64_t* in, int64_t n, uint64_t* out, void* cuda_stream);
 

@@ -48,6 +48,7 @@ def lib():
         L.gzo_fill_gaussians.argtypes = [ctypes.c_int, ctypes.c_int, P, i64, i64, i64, P, P, P, P, P, P, P,
                                          i64, ctypes.c_int]
         L.gzo_fill_u64.argtypes = [ctypes.c_int, i64, i64, i64, P, P, P]
+        L.gzo_occupancy.argtypes = [ctypes.c_int, ctypes.c_int, P, P, P, i64, P, P, i64]
         L.gzo_mutate.argtypes = [P, i64, i64, i64, P, P, P, P, ctypes.c_int, i64, ctypes.c_int]
         L.gzo_checksum.argtypes = [P, i64]
         L.gzo_checksum.restype = ctypes.c_uint64
@@ -121,6 +122,18 @@ def fill_gaussians(alg, source, states, n_per, spare=None, has=None, layers=None
                                       n_per, n_per, _p(states), _p(st_out), _p(spare), _p(has),
                                       _p(spare_out), _p(has_out), _p(out), guard, nthreads)
     return out, st_out, spare_out, has_out, status
+
+
+def occupancy(alg, source, state_words, n_calls, layers=None, guard=GUARD):
+    """One stream's sample_with_occupancy (samplers.py:89-93): (deviates, counts, state_out, status)."""
+    st = np.ascontiguousarray(state_words, dtype=np.uint64)
+    st_out = np.empty_like(st)
+    t = tables(layers or default_layers(alg))
+    out = np.zeros(max(n_calls, 1))
+    counts = np.zeros(t.n, dtype=np.uint64)
+    status = lib().gzo_occupancy(ALG[alg], SRC[source], ctypes.byref(t.raw), _p(st), _p(st_out), n_calls, _p(out),
+                                 _p(counts), guard)
+    return out[:n_calls], counts, st_out, status
 
 
 def fill_u64(source, states, n_per):

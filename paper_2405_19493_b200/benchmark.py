@@ -41,6 +41,20 @@ class BenchConfig:
     seed: int = DEFAULT_SEED
     confidence: float = 0.999
 
+    def __post_init__(self):
+        if self.measure_iters < 2:
+            raise ValueError("need at least 2 measurement iterations for a CI")
+        if self.warmup_iters < 0:
+            raise ValueError("warmup_iters must be >= 0")
+        if self.streams < 1 or self.per_stream < 1:
+            raise ValueError("streams and per_stream must be >= 1")
+        if not 0.0 < self.confidence < 1.0:
+            raise ValueError("confidence must be in (0, 1)")
+
+    @classmethod
+    def paper(cls, seed: int = DEFAULT_SEED) -> "BenchConfig":
+        return cls(warmup_iters=5, measure_iters=20, streams=1 << 20, per_stream=256, seed=seed)
+
     @classmethod
     def smoke(cls, seed: int = DEFAULT_SEED) -> "BenchConfig":
         return cls(warmup_iters=1, measure_iters=3, streams=1 << 12, seed=seed)
@@ -61,6 +75,18 @@ class BenchResult:
 
     def to_dict(self) -> dict:
         return asdict(self)
+
+
+@dataclass
+class ComparisonRow:
+    """Percent-faster relation between two results on the same source (bench.py:106-115)."""
+
+    baseline: BenchResult
+    candidate: BenchResult
+    percent_faster: float = field(init=False)
+
+    def __post_init__(self):
+        self.percent_faster = percent_faster(self.baseline.ns_per_op, self.candidate.ns_per_op)
 
 
 def checksum_fold(buf) -> int:

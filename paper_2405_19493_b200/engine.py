@@ -193,6 +193,31 @@ def fill_gaussians(sampler: GaussianSampler, source: UniformSource, out, guard: 
         sampler.spare = float(spare_out[0]) if has_out[0] else None
 
 
+def fill_with_occupancy(sampler: GaussianSampler, source: UniformSource, n_calls: int, guard: int = DEFAULT_GUARD):
+    """n_calls ziggurat calls on the device by one thread, counting the layer of
+    every attempt (gz_zig_occupancy): returns (deviates list, counts list) and
+    advances `source` like the reference's sample_with_occupancy."""
+    import torch
+
+    L = _lib.load()
+    alg = _alg_of(sampler)
+    if alg == 0:
+        raise TypeError("layer occupancy is defined for the ziggurat samplers only")
+    if n_calls < 0:
+        raise ValueError(f"n_calls must be >= 0, got {n_calls}")
+    st = _state_words(source)
+    src = _lib.SRC[source.source_id]
+    slot = table_slot(sampler.tables)
+    d_st = torch.from_numpy(st.view(np.int64)).to("cuda")
+    d_out = torch.empty(max(n_calls, 1), dtype=torch.float64, device="cuda")
+    d_cnt = torch.zeros(sampler.tables.n, dtype=torch.int64, device="cuda")
+    s = torch.cuda.current_stream().cuda_stream
+    check(L.gz_zig_occupancy(alg, src, slot, _ptr(d_st), _ptr(d_st), n_calls, _ptr(d_out), _ptr(d_cnt), guard, s))
+    check(L.gz_stream_check(s))
+    source.state = int(d_st.cpu().numpy().view(np.uint64)[0])
+    return d_out[:n_calls].cpu().tolist(), [int(c) for c in d_cnt.cpu().tolist()]
+
+
 def warm_up(sampler: GaussianSampler, source_id: str) -> None:
     """Upload tables and run one small fill so a timed region sees no first-use cost."""
     if not available():

@@ -56,6 +56,13 @@ class _ZigguratBase(GaussianSampler):
     def __init__(self, tables: ZigguratTables | None = None):
         self.tables = tables if tables is not None else _default_tables(self.default_layers)
 
+    def sample_with_occupancy(self, src, n_calls: int):
+        """(deviates, per-layer selection counts over all attempts) of n_calls
+        calls, advancing src (samplers.py:89-93, 138-142); run on the device."""
+        from . import engine
+
+        return engine.fill_with_occupancy(self, src, n_calls)
+
 
 _TABLE_CACHE: dict = {}
 

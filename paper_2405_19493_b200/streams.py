@@ -213,6 +213,11 @@ class MomentSummary:
     skewness: float
     excess_kurtosis: float
 
+    def to_json_dict(self) -> dict:
+        """stats.py:164-172 field layout."""
+        return {"test": "moments", "n": self.n, "mean": self.mean, "variance": self.variance,
+                "skewness": self.skewness, "excess_kurtosis": self.excess_kurtosis}
+
 
 def central_from_psum(psum, values_per_row: int, stream=None):
     """Deterministic device reduction of per-row power sums -> (n, mean, M2, M3, M4)."""

@@ -121,6 +121,14 @@ class GofReport:
     def passes(self, alpha: float) -> bool:
         return self.p_value > alpha
 
+    def verdict_at(self, alphas) -> dict:
+        return {a: self.passes(a) for a in alphas}
+
+    def to_json_dict(self, test: str, alpha: float, n: int, seed=None) -> dict:
+        """stats.py:189-199 field layout."""
+        return {"test": test, "statistic": self.statistic, "dof": self.dof, "p_value": self.p_value, "alpha": alpha,
+                "verdict": "pass" if self.passes(alpha) else "fail", "n": n, "seed": seed}
+
 
 @dataclass
 class KsReport:
@@ -132,6 +140,12 @@ class KsReport:
 
     def passes(self, alpha: float) -> bool:
         return self.d_statistic < self.critical_value(alpha)
+
+    def to_json_dict(self, alpha: float, seed=None) -> dict:
+        """stats.py:216-227 field layout."""
+        return {"test": "ks", "statistic": self.d_statistic, "dof": None, "p_value": None,
+                "critical_value": self.critical_value(alpha), "alpha": alpha,
+                "verdict": "pass" if self.passes(alpha) else "fail", "n": self.n, "seed": seed}
 
 
 # ---- device statistics --------------------------------------------------------------
@@ -189,6 +203,22 @@ def ks_test(x) -> KsReport:
     _check(L.gz_ks_stat(_p(xs), xs.numel(), _p(d), _stream(xs.device)))
     dp, dm = d.cpu().tolist()
     return KsReport(max(dp, dm), xs.numel())
+
+
+def moments(x):
+    """MomentSummary of x (float64 CUDA tensor) by device power sums
+    (gz_moments_buffer): stats.py:232-259 conventions (unbiased variance,
+    population excess kurtosis)."""
+    torch = _torch()
+    from .streams import summarize
+
+    L = _lib.load()
+    xs = x.reshape(-1).contiguous()
+    if xs.numel() < 4:
+        raise ValueError(f"moments requires n >= 4, got {xs.numel()}")
+    out5 = torch.empty(5, dtype=torch.float64, device=xs.device)
+    _check(L.gz_moments_buffer(_p(xs), xs.numel(), _p(out5), _stream(xs.device)))
+    return summarize(*out5.cpu().tolist())
 
 
 def uniform_counts_gof(counts) -> GofReport:

@@ -25,6 +25,12 @@ def golden():
         return json.load(f)
 
 
+@pytest.fixture(scope="session")
+def golden_cli():
+    with open(os.path.join(ROOT, "tests", "golden", "golden_cli.json")) as f:
+        return json.load(f)
+
+
 def hex_to_f64(hs):
     return np.array([int(h, 16) for h in hs], dtype=np.uint64).view(np.float64)
 
