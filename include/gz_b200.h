@@ -174,6 +174,16 @@ int gz_moments_buffer(const double* x, int64_t n, double* out5, void* cuda_strea
 int gz_zig_occupancy(int alg, int src, int table_slot, const uint64_t* state_in, uint64_t* state_out,
                      int64_t n_calls, double* out, uint64_t* counts, int64_t guard, void* cuda_stream);
 
+/*
+ * Self-check of the wedge pre-filters' error budget for a table slot: over n
+ * random wedge candidates, out3 (device f64[3]) = {max |y_f/y - 1|,
+ * max |e_f/e - 1| of the float exp2 filter, max |__expf/e - 1| of the warp
+ * kernels' filter}, e = the bit-exact glibc exp.  Both filters fall back to the
+ * exact test within 2^-15 of the accept boundary, so each maximum must stay
+ * well below 2^-16.  Test infrastructure; not on the generation path.
+ */
+int gz_wedge_filter_error(int table_slot, int64_t n, uint64_t seed, double* out3, void* cuda_stream);
+
 /* xor-fold of u64[n] (device) into *out (device): the global checksum. */
 int gz_xor_reduce(const uint64_t* in, int64_t n, uint64_t* out, void* cuda_stream);
 

@@ -6,6 +6,7 @@ fill_u64 with numpy or CUDA tensors, streams.*), i.e. through the C ABI of
 libgzb200.so; the oracle (oracle/gz_oracle.c) and the golden fixtures
 (tests/golden/golden.json, made by importing the reference) are the checkers.
 """
+import ctypes
 import hashlib
 import zlib
 
@@ -466,3 +467,23 @@ def test_benchmark_refuses_unsanctioned_pairing():
 
     with pytest.raises(gz.UnsanctionedPairing):
         B.run_benchmark("modified-ziggurat", "lcg48", B.BenchConfig.smoke())
+
+
+@pytest.mark.parametrize("layers", [8, 128, 256, 1024])
+def test_wedge_prefilter_error_budget(layers):
+    """The float/__expf wedge pre-filters fall back to the exact glibc exp within
+    2^-15 of the accept boundary; their measured errors must stay below 2^-17."""
+    from paper_2405_19493_b200 import _lib
+    from paper_2405_19493_b200.engine import table_slot
+    from paper_2405_19493_b200.samplers import _default_tables
+
+    L = _lib.load()
+    slot = table_slot(_default_tables(layers))
+    out = torch.zeros(3, dtype=torch.float64, device=DEV)
+    s = torch.cuda.current_stream().cuda_stream
+    _lib.check(L.gz_wedge_filter_error(slot, 1 << 24, 12345 + layers, ctypes.c_void_p(out.data_ptr()), s))
+    _lib.check(L.gz_stream_check(s))
+    ey, ef, ex = out.cpu().tolist()
+    assert 0 < ey < 2.0 ** -20
+    assert 0 < ef < 2.0 ** -17
+    assert 0 < ex < 2.0 ** -17
