@@ -184,6 +184,15 @@ int gz_zig_occupancy(int alg, int src, int table_slot, const uint64_t* state_in,
  */
 int gz_wedge_filter_error(int table_slot, int64_t n, uint64_t seed, double* out3, void* cuda_stream);
 
+/*
+ * Self-check of the branch-free correctly rounded divide and square root used by
+ * the polar drains, against div.rn / sqrt.rn, over n samples of the polar
+ * operand domain (s = v1^2 + v2^2 in (0, 1) incl. tiny s; a = -2 log s):
+ * counts2 (device u64[2]) = {quotient mismatches, sqrt mismatches}; both must
+ * be 0.  Test infrastructure; not on the generation path.
+ */
+int gz_polar_ops_selftest(int64_t n, uint64_t seed, uint64_t* counts2, void* cuda_stream);
+
 /* xor-fold of u64[n] (device) into *out (device): the global checksum. */
 int gz_xor_reduce(const uint64_t* in, int64_t n, uint64_t* out, void* cuda_stream);
 

@@ -487,3 +487,16 @@ def test_wedge_prefilter_error_budget(layers):
     assert 0 < ey < 2.0 ** -20
     assert 0 < ef < 2.0 ** -17
     assert 0 < ex < 2.0 ** -17
+
+
+def test_branch_free_divide_and_sqrt_are_correctly_rounded():
+    """The polar drains' divide/sqrt without special-case branches equal div.rn /
+    sqrt.rn bit for bit over 2^28 samples of the polar operand domain."""
+    from paper_2405_19493_b200 import _lib
+
+    L = _lib.load()
+    out = torch.zeros(2, dtype=torch.int64, device=DEV)
+    s = torch.cuda.current_stream().cuda_stream
+    _lib.check(L.gz_polar_ops_selftest(1 << 28, 20240531, ctypes.c_void_p(out.data_ptr()), s))
+    _lib.check(L.gz_stream_check(s))
+    assert out.cpu().tolist() == [0, 0]
