@@ -1,0 +1,463 @@
+/*
+ * gz_single.cuh -- one long stream decoded by the whole GPU (included by
+ * gz_engine.cu after its kernels and DevCtx).
+ *
+ * The reference's own API fills ONE stream per call (engine.fill_gaussians,
+ * engine.py:235-270; bench.py:201-215 times exactly that).  A warp per stream
+ * decodes about 0.1 G variates/s there, slower than the reference's CPU loop,
+ * so calls with one stream and many variates take this path instead:
+ *
+ *   polar  attempt j always consumes draws 2j and 2j+1 (samplers.py:185-192),
+ *          so the attempts are independent: count accepted attempts per block,
+ *          exclusive-scan the counts, and let every block transform and store
+ *          its accepted pairs at their prefix rank (stream compaction).
+ *   ziggurat  an attempt consumes 1 draw (fast path), 2 (wedge: the next draw
+ *          is its uniform) or 1 + 2t (tail, t pairs); which draws start attempts
+ *          is a chain 0 -> 0 + len(0) -> ...  Every draw position is classified
+ *          as if it started an attempt (len, accepted, value: independent), each
+ *          chunk of positions is walked from every possible entry offset
+ *          0..SZ_E-1 (the previous chunk's last attempt may overhang), the chunk
+ *          entries are linked in a prefix over chunks, and every chunk re-walks
+ *          from its true entry and stores its deviates at their prefix rank.
+ *
+ * Results are identical to the sequential loop by construction (same draws, same
+ * decisions, same order); tests compare them with the oracle and the golden
+ * fixtures.  Rare shapes this path does not cover (a tail overhanging more than
+ * SZ_E - 1 draws into the next chunk, a chunk with no accepted attempt, guards
+ * below SINGLE_MIN_GUARD) fall back to the warp-per-stream kernels.
+ */
+#pragma once
+
+constexpr int64_t SINGLE_MIN_N = 1 << 15;       /* below this the warp kernel is faster */
+constexpr int64_t SINGLE_MIN_GUARD = 1 << 13;   /* a guard trip needs a whole rejected chunk */
+constexpr int SP_T = 256;                       /* polar: attempts per block */
+constexpr int SZ_L = 2048;                      /* ziggurat: draw positions per chunk */
+constexpr int SZ_E = 8;                         /* ziggurat: entry offsets walked per chunk */
+
+/* (A, C) of n LCG steps (state -> A*state + C mod 2^48), by squaring */
+__device__ __forceinline__ void lcg_jump_n(uint64_t n, uint64_t& A, uint64_t& C)
+{
+    uint64_t a = GZ_LCG_A, c = GZ_LCG_C;
+    A = 1;
+    C = 0;
+    while (n) {
+        if (n & 1) {
+            C = (a * C + c) & GZ_MASK48;
+            A = (a * A) & GZ_MASK48;
+        }
+        c = (a * c + c) & GZ_MASK48;
+        a = (a * a) & GZ_MASK48;
+        n >>= 1;
+    }
+}
+
+/* the stream state after `draws` u64 draws from s0 (LCG: 2 steps per draw) */
+template <int SRC>
+__device__ __forceinline__ uint64_t single_state_at(uint64_t s0, uint64_t gam, uint64_t draws)
+{
+    if constexpr (SRC == 0) {
+        uint64_t A, C;
+        lcg_jump_n(2 * draws, A, C);
+        return (A * s0 + C) & GZ_MASK48;
+    } else {
+        return s0 + draws * gam;
+    }
+}
+
+/* ------------------------------------------------------------------ polar */
+
+/* per-block state base (thread 0) and per-thread offset (4t LCG steps / 2t draws) */
+template <int SRC>
+__device__ __forceinline__ uint64_t polar_single_state(const uint64_t* st0, uint64_t& gam, int64_t j0, uint64_t* s_base)
+{
+    const int t = threadIdx.x;
+    uint64_t s0;
+    if constexpr (SRC == 0) {
+        s0 = st0[0];
+        gam = 0;
+    } else {
+        s0 = st0[0];
+        gam = st0[1];
+    }
+    if constexpr (SRC == 0) {
+        if (t == 0) *s_base = single_state_at<0>(s0, 0, 2 * (uint64_t)j0);
+        __syncthreads();
+        uint64_t A, C;
+        lcg_jump_n(4 * (uint64_t)t, A, C);
+        return (A * *s_base + C) & GZ_MASK48;
+    } else {
+        return s0 + (uint64_t)(2 * (j0 + t)) * gam;
+    }
+}
+
+/* one polar attempt from state S (the state before its first draw): v1, v2, s and
+   the state after its two draws */
+template <int SRC>
+__device__ __forceinline__ bool polar_single_attempt(uint64_t S, uint64_t gam, double& v1, double& v2, double& s,
+                                                     uint64_t& S_after)
+{
+    const uint64_t ua = gz_next_seq<SRC>(S, gam);
+    const uint64_t ub = gz_next_seq<SRC>(S, gam);
+    S_after = S;
+    v1 = gz_unit53_pm1(ua);
+    v2 = gz_unit53_pm1(ub);
+    s = __dadd_rn(__dmul_rn(v1, v1), __dmul_rn(v2, v2));
+    return s > 0.0 && s < 1.0;
+}
+
+/* pass 1: accepted attempts per block for attempts [j0, j0 + n_att) */
+template <int SRC>
+__global__ void __launch_bounds__(SP_T) k_polar_single_count(const uint64_t* st0, int64_t j0, int64_t n_att, int* cnt)
+{
+    __shared__ uint64_t s_base;
+    __shared__ int s_c[SP_T / 32];
+    const int64_t jb = j0 + (int64_t)blockIdx.x * SP_T;
+    uint64_t gam;
+    const uint64_t S = polar_single_state<SRC>(st0, gam, jb, &s_base);
+    double v1, v2, s;
+    uint64_t Sa;
+    const bool acc = (jb + threadIdx.x < j0 + n_att) && polar_single_attempt<SRC>(S, gam, v1, v2, s, Sa);
+    const int wc = __popc(__ballot_sync(GZ_FULL, acc));
+    if ((threadIdx.x & 31) == 0) s_c[threadIdx.x >> 5] = wc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int tot = 0;
+        for (int w = 0; w < SP_T / 32; ++w) tot += s_c[w];
+        cnt[blockIdx.x] = tot;
+    }
+}
+
+struct PolarSingleOut {
+    double* out;           /* deviate 0 of the call (after a cached spare) */
+    int64_t pairs_done;    /* pairs stored by earlier segments */
+    int64_t np;            /* pairs the call needs */
+    bool odd;              /* the last pair's second value is the new spare */
+    double* spare_out;
+    uint64_t* state_out;
+};
+
+/* pass 2: transform and store the accepted pairs at their prefix rank */
+template <int SRC>
+__global__ void __launch_bounds__(SP_T) k_polar_single_emit(const uint64_t* st0, int64_t j0, int64_t n_att,
+                                                            const int* prefix, PolarSingleOut o)
+{
+    __shared__ uint64_t s_base;
+    __shared__ int s_c[SP_T / 32];
+    __shared__ uint64_t s_log[256];
+    const int64_t pre = prefix[blockIdx.x];
+    const int64_t need = o.np - o.pairs_done;
+    if (pre >= need) return;   /* block-uniform */
+    for (int i = threadIdx.x; i < 256; i += SP_T) s_log[i] = g_log_tab[i];
+    const int64_t jb = j0 + (int64_t)blockIdx.x * SP_T;
+    uint64_t gam;
+    const uint64_t S = polar_single_state<SRC>(st0, gam, jb, &s_base);
+    double v1, v2, s;
+    uint64_t Sa;
+    const bool acc = (jb + threadIdx.x < j0 + n_att) && polar_single_attempt<SRC>(S, gam, v1, v2, s, Sa);
+    const uint32_t bal = __ballot_sync(GZ_FULL, acc);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) s_c[wid] = __popc(bal);
+    __syncthreads();
+    int wbase = 0;
+    for (int w = 0; w < wid; ++w) wbase += s_c[w];
+    const int64_t rank = pre + wbase + __popc(bal & ((1u << lane) - 1u));
+    if (acc && rank < need) {
+        const int64_t k = o.pairs_done + rank;   /* the call's pair index */
+        const double mul = polar_mul(s, s_log);
+        const double o1 = __dmul_rn(v1, mul), o2 = __dmul_rn(v2, mul);
+        if (o.odd && k == o.np - 1) {
+            o.out[2 * k] = o1;
+            if (o.spare_out) o.spare_out[0] = o2;
+        } else {
+            pair_store(o.out + 2 * k, o1, o2);
+        }
+        if (rank == need - 1) {
+            /* the call's last attempt: the stream continues after its two draws */
+            if constexpr (SRC == 0) {
+                o.state_out[0] = Sa & GZ_MASK48;
+            } else {
+                o.state_out[0] = Sa;
+                o.state_out[1] = gam;
+            }
+        }
+    }
+}
+
+/* ------------------------------------------------------------------ ziggurat */
+
+/* a position classified as an attempt start: draws consumed, accepted, value */
+struct ZigPos {
+    uint16_t len;          /* 1 fast, 2 wedge, 1 + 2t tail; 0: tail guard tripped */
+    uint8_t acc;
+    uint8_t pad;
+};
+
+template <int SRC, bool MOD>
+__global__ void __launch_bounds__(256) k_zig_single_classify(const uint64_t* st0, int64_t p0, int64_t n_pos,
+                                                             const ulonglong2* kw, const double2* yd, int n_layers,
+                                                             double r, int64_t guard, ZigPos* pos, double* val)
+{
+    __shared__ uint64_t s_base;
+    const int64_t pb = p0 + (int64_t)blockIdx.x * 256;
+    const int t = threadIdx.x;
+    uint64_t s0 = st0[0], gam = 0;
+    if constexpr (SRC == 1) gam = st0[1];
+    uint64_t S;   /* the state before position pb + t's draw */
+    if constexpr (SRC == 0) {
+        if (t == 0) s_base = single_state_at<0>(s0, 0, (uint64_t)pb);
+        __syncthreads();
+        uint64_t A, C;
+        lcg_jump_n(2 * (uint64_t)t, A, C);
+        S = (A * s_base + C) & GZ_MASK48;
+    } else {
+        S = s0 + (uint64_t)(pb + t) * gam;
+    }
+    const int64_t k = pb + t;
+    if (k >= p0 + n_pos) return;
+    int ib = 0;
+    while ((1 << (ib + 1)) <= n_layers) ++ib;
+    const uint32_t imask = (uint32_t)n_layers - 1u;
+    const int mbits = 63 - ib;
+    const uint64_t mmask = (1ULL << mbits) - 1ULL;
+    /* ZigguratSampler._draw one attempt (samplers.py:95-115 / 144-165) */
+    const uint64_t u = gz_next_seq<SRC>(S, gam);
+    uint32_t i;
+    uint64_t m;
+    bool neg;
+    if constexpr (MOD) {
+        i = (uint32_t)u & imask;
+        m = u >> (ib + 1);
+        neg = (u >> ib) & 1;
+    } else {
+        i = (uint32_t)(u >> mbits) & imask;
+        m = u & mmask;
+        neg = u >> 63;
+    }
+    const ulonglong2 kk = kw[i];
+    double x = __dmul_rn(__ull2double_rn(m), __longlong_as_double((long long)kk.y));
+    ZigPos zp{1, 1, 0};
+    if (m >= kk.x) {
+        if (i != 0) {
+            const uint64_t u2 = gz_next_seq<SRC>(S, gam);
+            const double y = __dadd_rn(yd[i].x, __dmul_rn(gz_unit53(u2), yd[i].y));
+            zp.len = 2;
+            zp.acc = wedge_exact(y, __dmul_rn(__dmul_rn(-0.5, x), x)) ? 1 : 0;
+        } else {
+            const TailOut to = tail_seq<SRC>(S, gam, r, guard);
+            if (to.k < 0 || 1 + 2 * (int64_t)to.k > 65535) {
+                zp.len = 0;   /* guard tripped or an overlong tail: the caller falls back */
+                zp.acc = 0;
+            } else {
+                zp.len = (uint16_t)(1 + 2 * to.k);
+                x = to.v;
+            }
+        }
+    }
+    pos[k - p0] = zp;
+    val[k - p0] = neg ? -x : x;
+}
+
+/* per chunk and entry offset e: where the walk leaves the chunk and what it found */
+struct ZigExit {
+    int32_t exit;          /* next attempt start - chunk end (>= 0) */
+    int32_t cnt;           /* accepted attempts started in the chunk */
+    int32_t bad;           /* a zero-length position (guard / overlong tail) on the walk */
+    int32_t pad;
+};
+
+/* walk every entry offset 0..SZ_E-1 of chunk blockIdx.x through the chunk (one warp
+   per chunk, lanes 0..SZ_E-1 walk); each walk also leaves the bitmap of its accepted
+   attempt starts (SZ_L bits) in bm, so the emit pass needs no walk */
+constexpr int SZ_W = SZ_L / 32;   /* bitmap words per chunk and entry */
+__global__ void __launch_bounds__(32) k_zig_single_exits(const ZigPos* pos, int64_t n_pos, ZigExit* ex, uint32_t* bm)
+{
+    __shared__ uint16_t s_len[SZ_L];
+    __shared__ uint8_t s_acc[SZ_L];
+    __shared__ uint32_t s_bm[SZ_E][SZ_W];
+    const int c = blockIdx.x;
+    const int64_t c0 = (int64_t)c * SZ_L;
+    const int nl = (int)(n_pos - c0 < SZ_L ? n_pos - c0 : SZ_L);
+    for (int i = threadIdx.x; i < SZ_L; i += 32) {
+        if (i < nl) {
+            const ZigPos zp = pos[c0 + i];
+            s_len[i] = zp.len;
+            s_acc[i] = zp.acc;
+        }
+    }
+    for (int i = threadIdx.x; i < SZ_E * SZ_W; i += 32) (&s_bm[0][0])[i] = 0u;
+    __syncwarp();
+    const int e = threadIdx.x;
+    if (e < SZ_E) {
+        int p = e, cnt = 0, bad = 0;
+        uint32_t word = 0;
+        int wi = 0;
+        while (p < nl) {
+            const int l = s_len[p];
+            if (l == 0) {
+                bad = 1;
+                break;
+            }
+            if (s_acc[p]) {
+                ++cnt;
+                const int w = p >> 5;
+                if (w != wi) {
+                    s_bm[e][wi] = word;
+                    word = 0;
+                    wi = w;
+                }
+                word |= 1u << (p & 31);
+            }
+            p += l;
+        }
+        s_bm[e][wi] = word;
+        ZigExit x;
+        x.exit = bad ? 0 : p - nl;
+        x.cnt = cnt;
+        x.bad = bad;
+        x.pad = 0;
+        ex[(int64_t)c * SZ_E + e] = x;
+    }
+    __syncwarp();
+    uint32_t* dst = bm + (int64_t)c * SZ_E * SZ_W;
+    for (int i = threadIdx.x; i < SZ_E * SZ_W; i += 32) dst[i] = (&s_bm[0][0])[i];
+}
+
+/* the chunk chain, three levels: LINK_B chunks per block composed for every entry,
+   blocks linked by one thread, chunk entries/bases expanded per block */
+constexpr int LINK_B = 128;
+
+struct ZigLinkF {
+    int32_t exit, bad;     /* bad: an entry >= SZ_E, a zero-count chunk or a bad walk on the way */
+    int64_t cnt;
+};
+
+__global__ void __launch_bounds__(32) k_zig_single_link_blocks(const ZigExit* ex, int n_chunks, ZigLinkF* fb)
+{
+    __shared__ ZigExit s_ex[LINK_B * SZ_E];
+    const int b = blockIdx.x;
+    const int c0 = b * LINK_B, c1 = min(c0 + LINK_B, n_chunks);
+    for (int i = threadIdx.x; i < (c1 - c0) * SZ_E; i += 32) s_ex[i] = ex[(int64_t)c0 * SZ_E + i];
+    __syncwarp();
+    const int e0 = threadIdx.x;
+    if (e0 >= SZ_E) return;
+    int e = e0, bad = 0;
+    int64_t cnt = 0;
+    for (int c = c0; c < c1; ++c) {
+        if (e >= SZ_E) {
+            bad = 1;
+            break;
+        }
+        const ZigExit x = s_ex[(c - c0) * SZ_E + e];
+        if (x.bad || x.cnt == 0) bad = 1;
+        cnt += x.cnt;
+        e = x.exit;
+    }
+    ZigLinkF f;
+    f.exit = e;
+    f.bad = bad;
+    f.cnt = cnt;
+    fb[(int64_t)b * SZ_E + e0] = f;
+}
+
+struct ZigLinkTop {
+    int64_t total;         /* accepted attempts of the whole segment from entry 0 */
+    int32_t exit;          /* next attempt start - segment end */
+    int32_t bad;
+};
+
+__global__ void k_zig_single_link_top(const ZigLinkF* fb, int n_blocks, int* b_entry, int64_t* b_base, ZigLinkTop* top)
+{
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    int e = 0, bad = 0;
+    int64_t base = 0;
+    for (int b = 0; b < n_blocks; ++b) {
+        b_entry[b] = e;
+        b_base[b] = base;
+        if (e >= SZ_E) {
+            bad = 1;
+            break;
+        }
+        const ZigLinkF f = fb[(int64_t)b * SZ_E + e];
+        bad |= f.bad;
+        base += f.cnt;
+        e = f.exit;
+    }
+    top->total = base;
+    top->exit = e;
+    top->bad = bad;
+}
+
+__global__ void __launch_bounds__(32) k_zig_single_link_expand(const ZigExit* ex, int n_chunks, const int* b_entry,
+                                                               const int64_t* b_base, int* entry, int64_t* base)
+{
+    __shared__ ZigExit s_ex[LINK_B * SZ_E];
+    const int b = blockIdx.x;
+    const int c0 = b * LINK_B, c1 = min(c0 + LINK_B, n_chunks);
+    for (int i = threadIdx.x; i < (c1 - c0) * SZ_E; i += 32) s_ex[i] = ex[(int64_t)c0 * SZ_E + i];
+    __syncwarp();
+    if (threadIdx.x != 0) return;
+    int e = b_entry[b];
+    int64_t bs = b_base[b];
+    for (int c = c0; c < c1; ++c) {
+        entry[c] = e < SZ_E ? e : -1;
+        base[c] = bs;
+        if (e >= SZ_E) {
+            e = SZ_E;
+            continue;
+        }
+        const ZigExit x = s_ex[(c - c0) * SZ_E + e];
+        bs += x.cnt;
+        e = x.exit;
+    }
+}
+
+struct ZigSingleOut {
+    double* out;           /* output index 0 of this segment */
+    int64_t need;          /* deviates this segment must still produce */
+    int64_t p0;            /* first draw position of the segment (absolute) */
+    uint64_t* state_out;   /* written by the block holding the last needed deviate */
+};
+
+/* chunk c stores the values of its accepted attempt starts (the bitmap of its true
+   entry) from output index base[c] on; one thread per bitmap word */
+template <int SRC>
+__global__ void __launch_bounds__(SZ_W) k_zig_single_emit(const ZigPos* pos, const double* val, int64_t n_pos,
+                                                          const uint32_t* bm, const int* entry, const int64_t* base,
+                                                          const uint64_t* st0, ZigSingleOut o)
+{
+    __shared__ int s_w[SZ_W / 32];
+    const int c = blockIdx.x;
+    const int64_t b0 = base[c];
+    const int e = entry[c];
+    if (b0 >= o.need || e < 0) return;   /* block-uniform */
+    const int64_t c0 = (int64_t)c * SZ_L;
+    const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+    uint32_t word = bm[((int64_t)c * SZ_E + e) * SZ_W + t];
+    const int mine = __popc(word);
+    int incl = mine;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const int v = __shfl_up_sync(GZ_FULL, incl, off);
+        if (lane >= off) incl += v;
+    }
+    if (lane == 31) s_w[wid] = incl;
+    __syncthreads();
+    int wbase = 0;
+    for (int w = 0; w < wid; ++w) wbase += s_w[w];
+    int64_t rank = b0 + wbase + incl - mine;
+    while (word && rank < o.need) {
+        const int bit = __ffs(word) - 1;
+        word &= word - 1;
+        const int64_t p = c0 + 32 * t + bit;
+        o.out[rank] = val[p];
+        if (rank == o.need - 1) {
+            /* the segment's last needed deviate: the stream continues after it */
+            const uint64_t s0 = st0[0];
+            const uint64_t gam = SRC == 1 ? st0[1] : 0;
+            const uint64_t draws = (uint64_t)(o.p0 + p + pos[p].len);
+            o.state_out[0] = single_state_at<SRC>(s0, gam, draws);
+            if (SRC == 1) o.state_out[1] = gam;
+        }
+        ++rank;
+    }
+}

@@ -500,3 +500,51 @@ def test_branch_free_divide_and_sqrt_are_correctly_rounded():
     _lib.check(L.gz_polar_ops_selftest(1 << 28, 20240531, ctypes.c_void_p(out.data_ptr()), s))
     _lib.check(L.gz_stream_check(s))
     assert out.cpu().tolist() == [0, 0]
+
+
+@pytest.mark.parametrize("source,alg", PAIRINGS)
+@pytest.mark.parametrize("n", [32768, 32769, 100001, (1 << 20) + 3])
+def test_single_long_stream_vs_oracle(source, alg, n):
+    """One stream, many deviates: the whole-GPU decode (gz_single.cuh) equals the
+    sequential reference loop, incl. polar spares in and out and the final state."""
+    rng = np.random.default_rng(zlib.crc32(f"single/{source}/{alg}/{n}".encode()))
+    if source == "lcg48":
+        st_np = rng.integers(0, 2 ** 48, size=1, dtype=np.uint64)
+    else:
+        st_np = rng.integers(0, 2 ** 63, size=(1, 2), dtype=np.uint64) * np.uint64(2) + np.uint64(1)
+    kw, sp, hs = {}, None, None
+    if alg == "polar":
+        hs = np.array([n % 2], dtype=np.uint8)
+        sp = np.array([0.25 * (n % 2)])
+        kw = dict(spare=torch.from_numpy(sp.copy()).to(DEV), has_spare=torch.from_numpy(hs.copy()).to(DEV))
+    st = dev_states(source, st_np)
+    out = torch.empty((1, n), dtype=torch.float64, device=DEV)
+    streams.fill_gaussians_streams(alg, source, st, out, **kw)
+    ref, ref_st, ref_sp, ref_has, status = O.fill_gaussians(alg, source, st_np, n, *((sp, hs) if alg == "polar" else (None, None)))
+    assert status == 0
+    got = out.cpu().numpy()
+    bad = np.nonzero(got.view(np.uint64) != ref.view(np.uint64))[1]
+    assert bad.size == 0, f"{bad.size} deviates differ, first at {bad[:5]}"
+    assert np.array_equal(u64(st).reshape(ref_st.shape), ref_st)
+    if alg == "polar":
+        assert np.array_equal(kw["has_spare"].cpu().numpy(), ref_has)
+        if ref_has[0]:
+            assert bits_equal(kw["spare"].cpu().numpy(), ref_sp)
+
+
+def test_single_long_stream_matches_warp_kernel():
+    """The same call through the warp-per-stream kernel (policy 'warp' disables the
+    whole-GPU decode) gives the same bits."""
+    for source, alg in PAIRINGS:
+        src = gz.make_source(source, 99)
+        a = torch.empty(200_000, dtype=torch.float64, device=DEV)
+        engine.fill_gaussians(gz.make_sampler(alg), src, a)
+        s_a = src.state
+        streams.set_kernel_policy("warp")
+        try:
+            src = gz.make_source(source, 99)
+            b = torch.empty(200_000, dtype=torch.float64, device=DEV)
+            engine.fill_gaussians(gz.make_sampler(alg), src, b)
+        finally:
+            streams.set_kernel_policy("auto")
+        assert torch.equal(a, b) and src.state == s_a, (source, alg)
