@@ -40,6 +40,11 @@ class BenchConfig:
     per_stream: int = 256        # deviates per stream per iteration
     seed: int = DEFAULT_SEED
     confidence: float = 0.999
+    # "streams": `streams` x `per_stream` deviates per iteration from independent streams;
+    # "single": the reference's own call shape (bench.py:199-203) -- one source,
+    # engine.fill_gaussians of `per_stream` deviates per call into a device buffer,
+    # state carried from call to call, per-call overhead included
+    layout: str = "streams"
 
     def __post_init__(self):
         if self.measure_iters < 2:
@@ -50,6 +55,8 @@ class BenchConfig:
             raise ValueError("streams and per_stream must be >= 1")
         if not 0.0 < self.confidence < 1.0:
             raise ValueError("confidence must be in (0, 1)")
+        if self.layout not in ("streams", "single"):
+            raise ValueError(f"unknown layout: {self.layout!r}")
 
     @classmethod
     def paper(cls, seed: int = DEFAULT_SEED) -> "BenchConfig":
@@ -58,6 +65,11 @@ class BenchConfig:
     @classmethod
     def smoke(cls, seed: int = DEFAULT_SEED) -> "BenchConfig":
         return cls(warmup_iters=1, measure_iters=3, streams=1 << 12, seed=seed)
+
+    @classmethod
+    def single(cls, seed: int = DEFAULT_SEED, batch: int = BATCH_OPS) -> "BenchConfig":
+        """The reference harness's exact call shape: one stream, `batch` deviates per call."""
+        return cls(warmup_iters=3, measure_iters=10, streams=1, per_stream=batch, seed=seed, layout="single")
 
 
 @dataclass
@@ -132,6 +144,8 @@ def run_benchmark(sampler_id: str, source_id: str, cfg: BenchConfig | None = Non
     witness = np.empty(WITNESS_OPS)
     engine.fill_gaussians(make_sampler(sampler_id), make_source(source_id, cfg.seed), witness)
     checksum = checksum_fold(witness)
+    if cfg.layout == "single":
+        return _run_single(sampler_id, source_id, cfg, checksum)
     # many independent streams per iteration
     scheme = "lcg_master_plus_id" if source_id == "lcg48" else "sm_output_of_master"
     st = S.seed_streams(scheme, cfg.seed, 0, cfg.streams)
@@ -157,6 +171,29 @@ def run_benchmark(sampler_id: str, source_id: str, cfg: BenchConfig | None = Non
     lo, hi = confidence_interval(per_iter, cfg.confidence)
     return BenchResult(sampler_id, source_id, sum(per_iter) / len(per_iter), 0.5 * (hi - lo), per_iter,
                        ops * cfg.measure_iters, checksum, cfg.seed, cfg.confidence, "cuda")
+
+
+def _run_single(sampler_id: str, source_id: str, cfg: BenchConfig, checksum: int) -> BenchResult:
+    """bench.py:217-244 on the GPU: fresh seed-determined stream, fills of per_stream
+    deviates per call through engine.fill_gaussians (device buffer), CUDA-event timed."""
+    import torch
+
+    buf = torch.empty(cfg.per_stream, dtype=torch.float64, device="cuda")
+    smp, src = make_sampler(sampler_id), make_source(source_id, cfg.seed)
+    for _ in range(cfg.warmup_iters):
+        engine.fill_gaussians(smp, src, buf)
+    smp, src = make_sampler(sampler_id), make_source(source_id, cfg.seed)
+    per_iter = []
+    for _ in range(cfg.measure_iters):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        engine.fill_gaussians(smp, src, buf)
+        e1.record()
+        e1.synchronize()
+        per_iter.append(e0.elapsed_time(e1) * 1e6 / cfg.per_stream)
+    lo, hi = confidence_interval(per_iter, cfg.confidence)
+    return BenchResult(sampler_id, source_id, sum(per_iter) / len(per_iter), 0.5 * (hi - lo), per_iter,
+                       cfg.per_stream * cfg.measure_iters, checksum, cfg.seed, cfg.confidence, "cuda")
 
 
 _CSV_HEADER = "source,sampler,ns_per_op,ci_half_width,iters,ops_total,seed"
@@ -193,8 +230,12 @@ def main(argv=None) -> int:
     ap.add_argument("--format", default="md", choices=["md", "csv", "json"])
     ap.add_argument("--seed", type=lambda v: int(v, 0), default=DEFAULT_SEED)
     ap.add_argument("--smoke", action="store_true")
+    ap.add_argument("--layout", default="streams", choices=["streams", "single"])
     args = ap.parse_args(argv)
-    cfg = BenchConfig.smoke(args.seed) if args.smoke else BenchConfig(seed=args.seed)
+    if args.layout == "single":
+        cfg = BenchConfig.single(args.seed)
+    else:
+        cfg = BenchConfig.smoke(args.seed) if args.smoke else BenchConfig(seed=args.seed)
     rows = [run_benchmark(alg, src, cfg) for src in ("lcg48", "splitmix")
             for alg in ("polar", "ziggurat", "modified-ziggurat") if (src, alg) != ("lcg48", "modified-ziggurat")]
     print(render_table(rows, args.format))

@@ -133,3 +133,13 @@ def test_bench_cli_smoke():
     assert code == 0 and len(docs) == 3
     assert all(d["engine_used"] == "cuda" and d["ns_per_op"] > 0 for d in docs)
     assert sum("percent_faster_vs_polar" in d for d in docs) == 2
+
+
+@pytest.mark.gpu
+def test_bench_single_layout_matches_witness(golden):
+    """The reference's one-stream call shape on the GPU: same checksum witness."""
+    from paper_2405_19493_b200 import benchmark
+
+    r = benchmark.run_benchmark("ziggurat", "splitmix", benchmark.BenchConfig.single())
+    assert r.ns_per_op > 0 and r.engine_used == "cuda"
+    assert "%016x" % r.checksum == golden["bench_witness"]["splitmix/ziggurat/%d" % benchmark.DEFAULT_SEED]
