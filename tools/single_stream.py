@@ -19,5 +19,8 @@ for n in (1 << 20, 1 << 24):
         t = time.perf_counter()
         engine.fill_gaussians(make_sampler(alg), make_source(src, 3), buf)
         dh = time.perf_counter() - t
+        t = time.perf_counter()
+        engine.fill_gaussians(make_sampler(alg), make_source(src, 4), buf)   # reused (touched) buffer
+        dr = time.perf_counter() - t
         print(f"n=2^{n.bit_length()-1} {src}/{alg}: device out {dt*1e3:.2f} ms ({dt/n*1e9:.2f} ns/var), "
-              f"numpy out {dh*1e3:.2f} ms ({dh/n*1e9:.2f} ns/var)", flush=True)
+              f"fresh numpy out {dh*1e3:.2f} ms ({dh/n*1e9:.2f} ns/var), reused numpy {dr*1e3:.2f} ms", flush=True)
