@@ -548,3 +548,22 @@ def test_single_long_stream_matches_warp_kernel():
         finally:
             streams.set_kernel_policy("auto")
         assert torch.equal(a, b) and src.state == s_a, (source, alg)
+
+
+@pytest.mark.parametrize("source,alg", [("lcg48", "polar"), ("splitmix", "ziggurat")])
+def test_large_numpy_output_staged_copy(source, alg):
+    """numpy outputs above 8 MiB go through the pinned staging pieces: same bits as a
+    device-tensor fill of the same stream, and a non-multiple of the piece size."""
+    n = (5 << 20) + 12345          # 40+ MiB: two 32 MiB pieces plus a tail
+    a = np.empty(n)
+    src_a = gz.make_source(source, 31337)
+    engine.fill_gaussians(gz.make_sampler(alg), src_a, a)
+    b = torch.empty(n, dtype=torch.float64, device=DEV)
+    src_b = gz.make_source(source, 31337)
+    engine.fill_gaussians(gz.make_sampler(alg), src_b, b)
+    assert bits_equal(a, b.cpu().numpy()) and src_a.state == src_b.state
+    ref, ref_st, *_ = O.fill_gaussians(alg, source, np.array([[src_a.state, 0]], dtype=np.uint64)[:, :1]
+                                       if source == "lcg48" else np.array([[src_a.state, src_a.gamma]], dtype=np.uint64), 1000)
+    c = np.empty(1000)
+    engine.fill_gaussians(gz.make_sampler(alg), src_a, c)
+    assert bits_equal(c, ref[0])
