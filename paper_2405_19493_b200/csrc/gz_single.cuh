@@ -31,7 +31,7 @@
 constexpr int64_t SINGLE_MIN_N = 1 << 15;       /* below this the warp kernel is faster */
 constexpr int64_t SINGLE_MIN_GUARD = 1 << 13;   /* a guard trip needs a whole rejected chunk */
 constexpr int SP_T = 256;                       /* polar: attempts per block */
-constexpr int SZ_L = 2048;                      /* ziggurat: draw positions per chunk */
+constexpr int SZ_L = 1024;                      /* ziggurat: draw positions per chunk (= 32 bitmap words) */
 constexpr int SZ_E = 8;                         /* ziggurat: entry offsets walked per chunk */
 
 /* (A, C) of n LCG steps (state -> A*state + C mod 2^48), by squaring */
@@ -269,47 +269,73 @@ struct ZigExit {
    per chunk, lanes 0..SZ_E-1 walk); each walk also leaves the bitmap of its accepted
    attempt starts (SZ_L bits) in bm, so the emit pass needs no walk */
 constexpr int SZ_W = SZ_L / 32;   /* bitmap words per chunk and entry */
-__global__ void __launch_bounds__(32) k_zig_single_exits(const ZigPos* pos, int64_t n_pos, ZigExit* ex, uint32_t* bm)
+static_assert(SZ_W == 32, "the emit pass maps one bitmap word per lane");
+constexpr int SZ_CPW = 4;   /* chunks per warp in the exits pass (SZ_E lanes each) */
+__global__ void __launch_bounds__(32) k_zig_single_exits(const ZigPos* pos, int64_t n_pos, int n_chunks, ZigExit* ex,
+                                                         uint32_t* bm)
 {
-    __shared__ uint16_t s_len[SZ_L];
-    __shared__ uint8_t s_acc[SZ_L];
-    __shared__ uint32_t s_bm[SZ_E][SZ_W];
-    const int c = blockIdx.x;
-    const int64_t c0 = (int64_t)c * SZ_L;
-    const int nl = (int)(n_pos - c0 < SZ_L ? n_pos - c0 : SZ_L);
-    for (int i = threadIdx.x; i < SZ_L; i += 32) {
-        if (i < nl) {
-            const ZigPos zp = pos[c0 + i];
-            s_len[i] = zp.len;
-            s_acc[i] = zp.acc;
+    /* padded against bank conflicts: the groups' walks read rows SZ_L + 16 apart, the
+       lanes' bitmap rows are SZ_W + 1 words apart */
+    __shared__ uint16_t s_pk[SZ_CPW][SZ_L + 16];   /* len | acc << 15 */
+    __shared__ uint32_t s_bm[SZ_CPW][SZ_E][SZ_W + 1];
+    const int lane = threadIdx.x;
+    for (int g = 0; g < SZ_CPW; ++g) {
+        const int c = blockIdx.x * SZ_CPW + g;
+        if (c >= n_chunks) break;
+        const int64_t c0 = (int64_t)c * SZ_L;
+        const int nl = (int)(n_pos - c0 < SZ_L ? n_pos - c0 : SZ_L);
+        if (nl == SZ_L) {
+            /* 16-byte loads: four positions per lane and step */
+            const uint4* src = reinterpret_cast<const uint4*>(pos + c0);
+#pragma unroll
+            for (int it = 0; it < SZ_L / 4 / 32; ++it) {
+                const int q = it * 32 + lane;
+                const uint4 v = src[q];
+                const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const uint32_t len = w[k] & 0xFFFFu, acc = (w[k] >> 16) & 0xFFu;
+                    s_pk[g][4 * q + k] = (uint16_t)(len > 0x7FFFu ? 0u : (len | (acc ? 0x8000u : 0u)));
+                }
+            }
+        } else {
+            for (int i = lane; i < nl; i += 32) {
+                const ZigPos zp = pos[c0 + i];
+                s_pk[g][i] = (uint16_t)(zp.len > 0x7FFF ? 0 : (zp.len | (zp.acc ? 0x8000 : 0)));
+            }
         }
+#pragma unroll
+        for (int e = 0; e < SZ_E; ++e) s_bm[g][e][lane] = 0u;
     }
-    for (int i = threadIdx.x; i < SZ_E * SZ_W; i += 32) (&s_bm[0][0])[i] = 0u;
     __syncwarp();
-    const int e = threadIdx.x;
-    if (e < SZ_E) {
-        int p = e, cnt = 0, bad = 0;
-        uint32_t word = 0;
-        int wi = 0;
+    /* lane = SZ_E * g + e walks entry e of chunk g */
+    const int g = lane / SZ_E, e = lane % SZ_E;
+    const int c = blockIdx.x * SZ_CPW + g;
+    if (c < n_chunks) {
+        const int64_t c0 = (int64_t)c * SZ_L;
+        const int nl = (int)(n_pos - c0 < SZ_L ? n_pos - c0 : SZ_L);
+        const uint16_t* pk = s_pk[g];
+        uint32_t* bmw = s_bm[g][e];
+        int p = e, cnt = 0, bad = 0, cw = 0;
+        uint32_t word = 0;   /* bitmap word cw, stored when the walk leaves it */
         while (p < nl) {
-            const int l = s_len[p];
+            const uint32_t v = pk[p];
+            const int l = (int)(v & 0x7FFFu);
             if (l == 0) {
                 bad = 1;
                 break;
             }
-            if (s_acc[p]) {
-                ++cnt;
-                const int w = p >> 5;
-                if (w != wi) {
-                    s_bm[e][wi] = word;
-                    word = 0;
-                    wi = w;
-                }
-                word |= 1u << (p & 31);
+            const uint32_t acc = v >> 15;
+            cnt += (int)acc;
+            if ((p >> 5) != cw) {
+                bmw[cw] = word;
+                cw = p >> 5;
+                word = 0;
             }
+            word |= acc << (p & 31);
             p += l;
         }
-        s_bm[e][wi] = word;
+        bmw[cw] = word;
         ZigExit x;
         x.exit = bad ? 0 : p - nl;
         x.cnt = cnt;
@@ -318,8 +344,13 @@ __global__ void __launch_bounds__(32) k_zig_single_exits(const ZigPos* pos, int6
         ex[(int64_t)c * SZ_E + e] = x;
     }
     __syncwarp();
-    uint32_t* dst = bm + (int64_t)c * SZ_E * SZ_W;
-    for (int i = threadIdx.x; i < SZ_E * SZ_W; i += 32) dst[i] = (&s_bm[0][0])[i];
+    for (int g2 = 0; g2 < SZ_CPW; ++g2) {
+        const int c2 = blockIdx.x * SZ_CPW + g2;
+        if (c2 >= n_chunks) break;
+        uint32_t* dst = bm + (int64_t)c2 * SZ_E * SZ_W;
+#pragma unroll
+        for (int e2 = 0; e2 < SZ_E; ++e2) dst[e2 * SZ_W + lane] = s_bm[g2][e2][lane];
+    }
 }
 
 /* the chunk chain, three levels: LINK_B chunks per block composed for every entry,
@@ -365,9 +396,14 @@ struct ZigLinkTop {
     int32_t bad;
 };
 
-__global__ void k_zig_single_link_top(const ZigLinkF* fb, int n_blocks, int* b_entry, int64_t* b_base, ZigLinkTop* top)
+/* one block: the blocks' composed functions staged in shared memory, linked by one thread */
+__global__ void __launch_bounds__(256) k_zig_single_link_top(const ZigLinkF* fb, int n_blocks, int* b_entry,
+                                                             int64_t* b_base, ZigLinkTop* top)
 {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    extern __shared__ ZigLinkF s_fb[];
+    for (int i = threadIdx.x; i < n_blocks * SZ_E; i += blockDim.x) s_fb[i] = fb[i];
+    __syncthreads();
+    if (threadIdx.x != 0) return;
     int e = 0, bad = 0;
     int64_t base = 0;
     for (int b = 0; b < n_blocks; ++b) {
@@ -377,7 +413,7 @@ __global__ void k_zig_single_link_top(const ZigLinkF* fb, int n_blocks, int* b_e
             bad = 1;
             break;
         }
-        const ZigLinkF f = fb[(int64_t)b * SZ_E + e];
+        const ZigLinkF f = s_fb[b * SZ_E + e];
         bad |= f.bad;
         base += f.cnt;
         e = f.exit;
@@ -419,20 +455,21 @@ struct ZigSingleOut {
 };
 
 /* chunk c stores the values of its accepted attempt starts (the bitmap of its true
-   entry) from output index base[c] on; one thread per bitmap word */
+   entry) from output index base[c] on; one warp per chunk, one bitmap word per lane */
 template <int SRC>
-__global__ void __launch_bounds__(SZ_W) k_zig_single_emit(const ZigPos* pos, const double* val, int64_t n_pos,
-                                                          const uint32_t* bm, const int* entry, const int64_t* base,
-                                                          const uint64_t* st0, ZigSingleOut o)
+__global__ void __launch_bounds__(32) k_zig_single_emit(const ZigPos* pos, const double* val, int64_t n_pos,
+                                                        const uint32_t* bm, const int* entry, const int64_t* base,
+                                                        const uint64_t* st0, const ZigLinkTop* top, ZigSingleOut o)
 {
-    __shared__ int s_w[SZ_W / 32];
     const int c = blockIdx.x;
     const int64_t b0 = base[c];
     const int e = entry[c];
-    if (b0 >= o.need || e < 0) return;   /* block-uniform */
+    /* warp-uniform; a bad segment writes nothing (the caller reruns the call on the
+       warp kernel) */
+    if (b0 >= o.need || e < 0 || top->bad) return;
     const int64_t c0 = (int64_t)c * SZ_L;
-    const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
-    uint32_t word = bm[((int64_t)c * SZ_E + e) * SZ_W + t];
+    const int lane = threadIdx.x;
+    uint32_t word = bm[((int64_t)c * SZ_E + e) * SZ_W + lane];
     const int mine = __popc(word);
     int incl = mine;
 #pragma unroll
@@ -440,15 +477,11 @@ __global__ void __launch_bounds__(SZ_W) k_zig_single_emit(const ZigPos* pos, con
         const int v = __shfl_up_sync(GZ_FULL, incl, off);
         if (lane >= off) incl += v;
     }
-    if (lane == 31) s_w[wid] = incl;
-    __syncthreads();
-    int wbase = 0;
-    for (int w = 0; w < wid; ++w) wbase += s_w[w];
-    int64_t rank = b0 + wbase + incl - mine;
+    int64_t rank = b0 + incl - mine;
     while (word && rank < o.need) {
         const int bit = __ffs(word) - 1;
         word &= word - 1;
-        const int64_t p = c0 + 32 * t + bit;
+        const int64_t p = c0 + 32 * lane + bit;
         o.out[rank] = val[p];
         if (rank == o.need - 1) {
             /* the segment's last needed deviate: the stream continues after it */

@@ -18,6 +18,7 @@ and without libgzb200.so or a CUDA device every call raises EngineUnavailable.
 from __future__ import annotations
 
 import ctypes
+import threading
 
 import numpy as np
 
@@ -106,6 +107,25 @@ def _state_words(source: UniformSource) -> np.ndarray:
     raise TypeError(f"no engine support for source {source.source_id!r} (the B200 engine has no CPU fallback)")
 
 
+_io = threading.local()
+
+
+def _io_words(dev):
+    """A pinned host int64[8] and a device int64[8] for one call's small inputs and
+    outputs (state in/out, spare in/out, flags), cached per thread and device:
+    one H2D and one D2H copy per call instead of five tensors."""
+    import torch
+
+    key = dev.index if dev.index is not None else torch.cuda.current_device()
+    cache = getattr(_io, "bufs", None)
+    if cache is None:
+        cache = _io.bufs = {}
+    if key not in cache:
+        cache[key] = (torch.zeros(8, dtype=torch.int64).pin_memory(),
+                      torch.zeros(8, dtype=torch.int64, device=torch.device("cuda", key)))
+    return cache[key]
+
+
 def _is_cuda_tensor(out) -> bool:
     return hasattr(out, "is_cuda") and bool(out.is_cuda)
 
@@ -162,21 +182,28 @@ def fill_gaussians(sampler: GaussianSampler, source: UniformSource, out, guard: 
         if out.dim() != 1 or not out.is_contiguous() or out.dtype != torch.float64:
             raise ValueError("out must be a contiguous 1-D float64 CUDA tensor")
         dev = out.device
-        d_st = torch.from_numpy(st.view(np.int64)).to(dev)
-        d_sp = torch.from_numpy(spare_in).to(dev)
-        d_hs = torch.from_numpy(has_in).to(dev)
-        d_spo = torch.zeros(1, dtype=torch.float64, device=dev)
-        d_hso = torch.zeros(1, dtype=torch.uint8, device=dev)
+        h, d = _io_words(dev)
+        hv = h.numpy()
+        hv[:] = 0
+        hv[:st.size] = st.view(np.int64)
+        if polar:
+            hv[4] = spare_in.view(np.int64)[0]
+            hv[5] = int(has_in[0])
+        d.copy_(h, non_blocking=True)
+        base = d.data_ptr()
         s = torch.cuda.current_stream(dev).cuda_stream
         n = out.numel()
-        check(L.gz_fill_gaussians(alg, src, slot, 1, n, n, _ptr(d_st), _ptr(d_st),
-                                  _ptr(d_sp) if polar else None, _ptr(d_hs) if polar else None,
-                                  _ptr(d_spo) if polar else None, _ptr(d_hso) if polar else None,
+        check(L.gz_fill_gaussians(alg, src, slot, 1, n, n, ctypes.c_void_p(base), ctypes.c_void_p(base + 16),
+                                  ctypes.c_void_p(base + 32) if polar else None,
+                                  ctypes.c_void_p(base + 40) if polar else None,
+                                  ctypes.c_void_p(base + 48) if polar else None,
+                                  ctypes.c_void_p(base + 56) if polar else None,
                                   _ptr(out), None, None, guard, s))
-        check(L.gz_stream_check(s))
-        st = d_st.cpu().numpy().view(np.uint64)
-        spare_out = d_spo.cpu().numpy()
-        has_out = d_hso.cpu().numpy()
+        h.copy_(d, non_blocking=True)
+        check(L.gz_stream_check(s))          # synchronises the stream: h holds the results
+        st = hv[2:2 + st.size].copy().view(np.uint64)
+        spare_out = hv[6:7].copy().view(np.float64)
+        has_out = np.array([hv[7] & 0xFF], dtype=np.uint8)
     else:
         buf = out if (isinstance(out, np.ndarray) and out.dtype == np.float64 and out.ndim == 1
                       and out.flags.c_contiguous) else np.empty(len(out), dtype=np.float64)
