@@ -494,3 +494,38 @@ __global__ void __launch_bounds__(32) k_zig_single_emit(const ZigPos* pos, const
         ++rank;
     }
 }
+
+/* ------------------------------------------------------------------ fill_u64 */
+
+/* u64 draws [0, n) of one stream (engine.fill_u64 on one source, engine.py:224-232),
+   one thread per draw: draw k is independent given the state after k draws */
+template <int SRC>
+__global__ void __launch_bounds__(256) k_u64_single(const uint64_t* st0, int64_t n, uint64_t* out)
+{
+    __shared__ uint64_t s_base;
+    const int64_t kb = (int64_t)blockIdx.x * 256;
+    const int t = threadIdx.x;
+    const uint64_t s0 = st0[0];
+    uint64_t S, gam = 0;
+    if constexpr (SRC == 0) {
+        if (t == 0) s_base = single_state_at<0>(s0, 0, (uint64_t)kb);
+        __syncthreads();
+        uint64_t A, C;
+        lcg_jump_n(2 * (uint64_t)t, A, C);
+        S = (A * s_base + C) & GZ_MASK48;
+    } else {
+        gam = st0[1];
+        S = s0 + (uint64_t)(kb + t) * gam;
+    }
+    if (kb + t < n) out[kb + t] = gz_next_seq<SRC>(S, gam);
+}
+
+/* the state after n draws (a separate launch: state_out may alias the input) */
+template <int SRC>
+__global__ void k_u64_single_state(const uint64_t* st0, int64_t n, uint64_t* state_out)
+{
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const uint64_t gam = SRC == 1 ? st0[1] : 0;
+    state_out[0] = single_state_at<SRC>(st0[0], gam, (uint64_t)n);
+    if (SRC == 1) state_out[1] = gam;
+}

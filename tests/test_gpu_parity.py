@@ -567,3 +567,18 @@ def test_large_numpy_output_staged_copy(source, alg):
     c = np.empty(1000)
     engine.fill_gaussians(gz.make_sampler(alg), src_a, c)
     assert bits_equal(c, ref[0])
+
+
+@pytest.mark.parametrize("source", ["lcg48", "splitmix"])
+@pytest.mark.parametrize("n", [32768, 1_000_003])
+def test_fill_u64_single_long_stream(source, n):
+    """engine.fill_u64 on one source: a thread per draw (gz_single.cuh) == the oracle."""
+    st_np = (np.array([[123456789]], dtype=np.uint64) if source == "lcg48"
+             else np.array([[987654321, O.GOLDEN_GAMMA]], dtype=np.uint64))
+    src = gz.make_source(source, 0)
+    src.state = int(st_np[0, 0])
+    out = torch.empty(n, dtype=torch.int64, device=DEV)
+    engine.fill_u64(src, out)
+    ref, ref_st = O.fill_u64(source, st_np[:, 0] if source == "lcg48" else st_np, n)
+    assert np.array_equal(out.cpu().numpy().view(np.uint64), ref[0])
+    assert src.state == int(ref_st.reshape(-1)[0])
