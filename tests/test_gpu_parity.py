@@ -582,3 +582,22 @@ def test_fill_u64_single_long_stream(source, n):
     ref, ref_st = O.fill_u64(source, st_np[:, 0] if source == "lcg48" else st_np, n)
     assert np.array_equal(out.cpu().numpy().view(np.uint64), ref[0])
     assert src.state == int(ref_st.reshape(-1)[0])
+
+
+@pytest.mark.parametrize("n", [40001, 65536])
+def test_polar_single_stream_host_path_with_spare(n):
+    """numpy output, cached spare in and out, one long stream (gz_fill_gaussians_host ->
+    the whole-GPU decode) against the per-call oracle semantics."""
+    smp = gz.make_sampler("polar")
+    src = gz.make_source("lcg48", 2024)
+    smp.spare = -0.75
+    buf = np.empty(n)
+    engine.fill_gaussians(smp, src, buf)
+    st0 = np.array([gz.make_source("lcg48", 2024).state], dtype=np.uint64)
+    ref, ref_st, ref_sp, ref_has, status = O.fill_gaussians("polar", "lcg48", st0, n, np.array([-0.75]),
+                                                             np.array([1], dtype=np.uint8))
+    assert status == 0 and bits_equal(buf, ref[0])
+    assert src.state == int(ref_st[0])
+    assert (smp.spare is not None) == bool(ref_has[0])
+    if ref_has[0]:
+        assert bits_equal(np.array([smp.spare]), ref_sp)
