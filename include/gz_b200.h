@@ -94,7 +94,11 @@ int gz_tables_upload(int slot, int n, const uint64_t* ktab, const double* wtab, 
  *               {sum x, sum x^2, sum x^3, sum x^4} for gz_moments_reduce
  *   guard       rejection-loop guard (GZ_DEFAULT_GUARD in the reference)
  *   cuda_stream cudaStream_t (NULL = legacy default stream)
- * Asynchronous: a tripped guard is reported by gz_stream_check().
+ * Asynchronous: a tripped guard is reported by gz_stream_check().  Exception: one
+ * stream of at least 2^15 deviates (the reference's engine.fill_gaussians call
+ * shape, no checksum/psum, guard >= 8192) is decoded by the whole GPU
+ * (csrc/gz_single.cuh) and synchronises `cuda_stream` once or twice inside the
+ * call; gz_set_kernel_policy(1) keeps the plain warp-per-stream schedule.
  */
 int gz_fill_gaussians(int alg, int src, int table_slot, int64_t n_streams, int64_t n_per, int64_t ld,
                       const uint64_t* state_in, uint64_t* state_out,
