@@ -601,3 +601,34 @@ def test_polar_single_stream_host_path_with_spare(n):
     assert (smp.spare is not None) == bool(ref_has[0])
     if ref_has[0]:
         assert bits_equal(np.array([smp.spare]), ref_sp)
+
+
+def test_single_stream_segments_hand_over():
+    """The single-stream decode in many small segments (GZ_SINGLE_SEG) gives the same
+    bits: each segment starts at the previous one's next attempt boundary."""
+    import subprocess
+    import sys
+
+    code = r"""
+import numpy as np, torch
+import paper_2405_19493_b200 as gz
+from paper_2405_19493_b200 import engine
+res = []
+for source, alg in (("lcg48", "polar"), ("splitmix", "ziggurat"), ("lcg48", "modified-ziggurat")):
+    out = torch.empty(300001, dtype=torch.float64, device="cuda")
+    src = gz.make_source(source, 77)
+    engine.fill_gaussians(gz.make_sampler(alg), src, out)
+    res.append((out.cpu().numpy().view(np.uint64).tobytes().hex()[:64], int(np.bitwise_xor.reduce(out.cpu().numpy().view(np.uint64))), src.state))
+print(repr(res))
+"""
+    import os
+
+    env = dict(os.environ)
+    outs = []
+    for seg in ("", "40000"):
+        env["GZ_SINGLE_SEG"] = seg
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                           cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(r.stdout.strip().splitlines()[-1])
+    assert outs[0] == outs[1]
