@@ -197,6 +197,13 @@ int gz_wedge_filter_error(int table_slot, int64_t n, uint64_t seed, double* out3
  */
 int gz_polar_ops_selftest(int64_t n, uint64_t seed, uint64_t* counts2, void* cuda_stream);
 
+/*
+ * One tail_sample(src, r) call (samplers.py:40-57): a deviate beyond r > 0 from the
+ * stream at `state` (device, 1 or 2 words, advanced in place) into *out (device).
+ * Guard trips are reported by gz_stream_check.
+ */
+int gz_tail_sample(int src, uint64_t* state, double r, int64_t guard, double* out, void* cuda_stream);
+
 /* xor-fold of u64[n] (device) into *out (device): the global checksum. */
 int gz_xor_reduce(const uint64_t* in, int64_t n, uint64_t* out, void* cuda_stream);
 

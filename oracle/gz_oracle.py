@@ -49,6 +49,7 @@ def lib():
                                          i64, ctypes.c_int]
         L.gzo_fill_u64.argtypes = [ctypes.c_int, i64, i64, i64, P, P, P]
         L.gzo_occupancy.argtypes = [ctypes.c_int, ctypes.c_int, P, P, P, i64, P, P, i64]
+        L.gzo_tail_sample.argtypes = [ctypes.c_int, P, P, ctypes.c_double, i64, P]
         L.gzo_mutate.argtypes = [P, i64, i64, i64, P, P, P, P, ctypes.c_int, i64, ctypes.c_int]
         L.gzo_checksum.argtypes = [P, i64]
         L.gzo_checksum.restype = ctypes.c_uint64
@@ -134,6 +135,15 @@ def occupancy(alg, source, state_words, n_calls, layers=None, guard=GUARD):
     status = lib().gzo_occupancy(ALG[alg], SRC[source], ctypes.byref(t.raw), _p(st), _p(st_out), n_calls, _p(out),
                                  _p(counts), guard)
     return out[:n_calls], counts, st_out, status
+
+
+def tail_sample(source, state_words, r, guard=GUARD):
+    """samplers.py:40-57 on one stream: (value, state_out, status)."""
+    st = np.ascontiguousarray(state_words, dtype=np.uint64)
+    st_out = np.empty_like(st)
+    out = np.zeros(1)
+    status = lib().gzo_tail_sample(SRC[source], _p(st), _p(st_out), float(r), guard, _p(out))
+    return float(out[0]), st_out, status
 
 
 def fill_u64(source, states, n_per):

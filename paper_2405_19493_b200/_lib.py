@@ -24,7 +24,7 @@ EXPORTS = ("gz_version", "gz_last_error", "gz_device_count", "gz_set_kernel_poli
            "gz_fill_unit_affine", "gz_mutate", "gz_moments_reduce", "gz_xor_reduce", "gz_stream_check",
            "gz_host_alloc", "gz_host_free", "gz_build_tables", "gz_hist_edges", "gz_ks_stat", "gz_lowbits_hist", "gz_libm_eval_device", "gz_libm_exp",
            "gz_libm_log", "gz_moments_buffer", "gz_zig_occupancy",
-           "gz_wedge_filter_error", "gz_polar_ops_selftest")
+           "gz_wedge_filter_error", "gz_polar_ops_selftest", "gz_tail_sample")
 
 
 class EngineUnavailable(RuntimeError):
@@ -76,6 +76,7 @@ def load(require_device: bool = True):
             L.gz_zig_occupancy.argtypes = [I, I, I, P, P, i64, P, P, i64, P]
             L.gz_wedge_filter_error.argtypes = [I, i64, ctypes.c_uint64, P, P]
             L.gz_polar_ops_selftest.argtypes = [i64, ctypes.c_uint64, P, P]
+            L.gz_tail_sample.argtypes = [I, P, D, i64, P, P]
             L.gz_libm_exp.argtypes = [D]
             L.gz_libm_exp.restype = D
             L.gz_libm_log.argtypes = [D]

@@ -18,7 +18,6 @@ from __future__ import annotations
 
 import json
 import math
-import statistics
 from dataclasses import asdict, dataclass, field
 
 import numpy as np
@@ -107,30 +106,43 @@ def checksum_fold(buf) -> int:
     return int(np.bitwise_xor.reduce(a.view(np.uint64))) if a.size else 0
 
 
-def _t_quantile(p: float, dof: int) -> float:
-    try:
-        from scipy.stats import t
+def student_t_quantile(confidence: float, dof: int) -> float:
+    """Two-sided Student-t quantile (bench.py:118-140): bisection of the t survival
+    function 0.5 * I_{dof/(dof+t^2)}(dof/2, 1/2)."""
+    from .verify import regularized_beta
 
-        return float(t.ppf(p, dof))
-    except Exception:  # pragma: no cover - normal approximation without scipy
-        from statistics import NormalDist
+    if not 0.0 < confidence < 1.0:
+        raise ValueError(f"confidence must be in (0, 1), got {confidence}")
+    if dof < 1:
+        raise ValueError(f"dof must be >= 1, got {dof}")
+    tail = 0.5 * (1.0 - confidence)
+    lo, hi = 0.0, 1e8
+    for _ in range(200):
+        mid = 0.5 * (lo + hi)
+        if 0.5 * regularized_beta(0.5 * dof, 0.5, dof / (dof + mid * mid)) > tail:
+            lo = mid
+        else:
+            hi = mid
+    return 0.5 * (lo + hi)
 
-        return NormalDist().inv_cdf(p)
 
-
-def confidence_interval(samples, confidence: float):
-    """Student-t interval of the mean (bench.py:143-152 conventions)."""
-    n = len(samples)
-    mean = sum(samples) / n
+def confidence_interval(xs, level: float):
+    """Two-sided Student-t interval (lo, hi) of the mean of xs (bench.py:143-152)."""
+    xs = list(xs)
+    n = len(xs)
     if n < 2:
-        return mean, mean
-    half = _t_quantile(0.5 + 0.5 * confidence, n - 1) * statistics.stdev(samples) / math.sqrt(n)
+        raise ValueError(f"confidence interval needs n >= 2, got {n}")
+    mean = sum(xs) / n
+    var = sum((x - mean) ** 2 for x in xs) / (n - 1)
+    half = student_t_quantile(level, n - 1) * math.sqrt(var / n)
     return mean - half, mean + half
 
 
-def percent_faster(slow_ns: float, fast_ns: float) -> float:
-    """How much faster `fast` is than `slow`, in percent of the slower time."""
-    return 100.0 * (slow_ns - fast_ns) / slow_ns
+def percent_faster(baseline_ns: float, candidate_ns: float) -> float:
+    """How much faster the candidate is than the baseline, in percent (bench.py:155-160)."""
+    if baseline_ns <= 0.0 or candidate_ns <= 0.0:
+        raise ValueError("ns/op inputs must be positive")
+    return 100.0 * (1.0 - candidate_ns / baseline_ns)
 
 
 def run_benchmark(sampler_id: str, source_id: str, cfg: BenchConfig | None = None) -> BenchResult:

@@ -286,3 +286,19 @@ __global__ void k_libm_eval(int fn, const double* in, double* out, int64_t n)
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
         out[k] = fn == 0 ? gz_exp_t(in[k], g_exp_tab) : gz_log_t(in[k], g_log_tab);
 }
+
+/* one tail_sample call (samplers.py:40-57) on one stream, by one thread */
+template <int SRC>
+__global__ void k_tail_sample(uint64_t* state, double r, int64_t guard, double* out)
+{
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const uint64_t gam = SRC == 1 ? state[1] : 0;
+    const TailOut to = tail_seq<SRC>(state[0], gam, r, guard);
+    if (to.k < 0) {
+        gz_raise(GZ_ERR_GUARD, 0);
+        return;
+    }
+    state[0] = SRC == 0 ? (to.st & GZ_MASK48) : to.st;
+    out[0] = to.v;
+}
+

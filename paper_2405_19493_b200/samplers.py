@@ -9,6 +9,7 @@ one-element fill, `sample(src, n)` an n-element fill.  The pairing gate
 from __future__ import annotations
 
 import abc
+import ctypes
 
 import numpy as np
 
@@ -22,6 +23,28 @@ _UNSAFE_PAIRINGS = {("lcg48", "modified-ziggurat")}
 __all__ = ["LOOP_GUARD", "SAMPLER_IDS", "GaussianSampler", "ZigguratSampler", "ModifiedZigguratSampler",
            "PolarSampler", "RejectionLoopExceeded", "UnsanctionedPairing", "gaussian_affine", "is_sanctioned",
            "require_sanctioned", "make_sampler"]
+
+
+def tail_sample(src, r: float, guard: int = LOOP_GUARD) -> float:
+    """One deviate from the normal tail beyond r > 0 (samplers.py:40-57), drawn from
+    `src` on the device (one thread); advances src like the reference."""
+    import torch
+
+    from . import engine
+    from ._lib import SRC, check, load
+
+    if not r > 0.0:
+        raise ValueError(f"tail boundary must be positive, got {r}")
+    L = load()
+    st = engine._state_words(src)
+    d = torch.from_numpy(st.view(np.int64).copy()).to("cuda")
+    out = torch.zeros(1, dtype=torch.float64, device="cuda")
+    s = torch.cuda.current_stream().cuda_stream
+    check(L.gz_tail_sample(SRC[src.source_id], ctypes.c_void_p(d.data_ptr()), float(r), guard,
+                           ctypes.c_void_p(out.data_ptr()), s))
+    check(L.gz_stream_check(s))
+    src.state = int(d.cpu().numpy().view(np.uint64)[0])
+    return float(out.cpu()[0])
 
 
 class UnsanctionedPairing(ValueError):

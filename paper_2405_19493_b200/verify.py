@@ -112,6 +112,48 @@ def chi_square_sf(statistic: float, dof: int) -> float:
     return h * math.exp(log_pref)
 
 
+def _beta_continued_fraction(a: float, b: float, x: float) -> float:
+    """The continued fraction of I_x(a, b) (modified Lentz evaluation)."""
+    tiny = 1e-300
+    apb, ap1, am1 = a + b, a + 1.0, a - 1.0
+    c, d = 1.0, 1.0 - apb * x / ap1
+    d = 1.0 / (tiny if abs(d) < tiny else d)
+    h = d
+    for m in range(1, 300):
+        m2 = 2 * m
+        for num in (m * (b - m) * x / ((am1 + m2) * (a + m2)),
+                    -(a + m) * (apb + m) * x / ((a + m2) * (ap1 + m2))):
+            d = 1.0 + num * d
+            d = 1.0 / (tiny if abs(d) < tiny else d)
+            c = 1.0 + num / c
+            c = tiny if abs(c) < tiny else c
+            h *= d * c
+        if abs(d * c - 1.0) < 1e-16:
+            break
+    return h
+
+
+def regularized_beta(a: float, b: float, x: float) -> float:
+    """Regularized incomplete beta I_x(a, b) (the reference's stats.py:137-151 helper)."""
+    if x <= 0.0:
+        return 0.0
+    if x >= 1.0:
+        return 1.0
+    front = math.exp(math.lgamma(a + b) - math.lgamma(a) - math.lgamma(b) + a * math.log(x) + b * math.log1p(-x))
+    if x < (a + 1.0) / (a + b + 2.0):
+        return front * _beta_continued_fraction(a, b, x) / a
+    return 1.0 - front * _beta_continued_fraction(b, a, 1.0 - x) / b
+
+
+def _as_device(x):
+    """A float64 CUDA tensor view of x (CUDA tensors pass through; numpy arrays and
+    sequences are copied to the device -- the statistics then run there)."""
+    torch = _torch()
+    if hasattr(x, "is_cuda") and x.is_cuda:
+        return x
+    return torch.as_tensor(np.ascontiguousarray(x, dtype=np.float64), device="cuda")
+
+
 @dataclass
 class GofReport:
     statistic: float
@@ -155,7 +197,7 @@ def histogram(x, edges) -> np.ndarray:
     edges, numpy.searchsorted(edges, x, side='right') semantics.  Exact."""
     torch = _torch()
     L = _lib.load()
-    xs = x.reshape(-1).contiguous()
+    xs = _as_device(x).reshape(-1).contiguous()
     e = torch.tensor(sorted(float(v) for v in edges), dtype=torch.float64, device=xs.device)
     counts = torch.zeros(e.numel() + 1, dtype=torch.int64, device=xs.device)
     s = _stream(xs.device)
@@ -198,7 +240,7 @@ def ks_test(x) -> KsReport:
     """Two-sided KS distance of x against N(0,1) (device sort + reduction)."""
     torch = _torch()
     L = _lib.load()
-    xs = x.reshape(-1).contiguous()
+    xs = _as_device(x).reshape(-1).contiguous()
     d = torch.zeros(2, dtype=torch.float64, device=xs.device)
     _check(L.gz_ks_stat(_p(xs), xs.numel(), _p(d), _stream(xs.device)))
     dp, dm = d.cpu().tolist()
@@ -206,14 +248,14 @@ def ks_test(x) -> KsReport:
 
 
 def moments(x):
-    """MomentSummary of x (float64 CUDA tensor) by device power sums
+    """MomentSummary of x (float64 CUDA tensor, or any float sequence) by device power sums
     (gz_moments_buffer): stats.py:232-259 conventions (unbiased variance,
     population excess kurtosis)."""
     torch = _torch()
     from .streams import summarize
 
     L = _lib.load()
-    xs = x.reshape(-1).contiguous()
+    xs = _as_device(x).reshape(-1).contiguous()
     if xs.numel() < 4:
         raise ValueError(f"moments requires n >= 4, got {xs.numel()}")
     out5 = torch.empty(5, dtype=torch.float64, device=xs.device)

@@ -16,7 +16,8 @@ import sys
 
 import numpy as np
 
-from gausszig import cli, make_sampler, make_source
+from gausszig import bench, cli, make_sampler, make_source
+from gausszig.stats import regularized_beta
 
 OUT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden_cli.json")
 
@@ -56,6 +57,17 @@ def main():
                     "state": "%016x" % src.state})
     for argv in SAMPLE_ARGS:
         g["cli"].append(run_cli(argv))
+    # bench.py / stats.py host helpers (student_t_quantile, confidence_interval,
+    # percent_faster, regularized_beta)
+    g["host_fns"] = {
+        "t_quantile": [[c, d, bench.student_t_quantile(c, d).hex()]
+                       for c in (0.5, 0.9, 0.95, 0.999) for d in (1, 2, 3, 9, 30, 200)],
+        "ci": [[xs, lvl, [v.hex() for v in bench.confidence_interval(xs, lvl)]]
+               for xs, lvl in (([1.0, 1.2, 0.9, 1.1], 0.999), ([3.25, 3.5, 3.0], 0.9))],
+        "percent_faster": [[b, c, bench.percent_faster(b, c).hex()] for b, c in ((5.0, 3.0), (1.7, 2.9))],
+        "beta": [[a, b, x, regularized_beta(a, b, x).hex()]
+                 for a, b, x in ((0.5, 0.5, 0.3), (2.0, 3.0, 0.7), (15.0, 0.5, 0.99), (0.5, 7.0, 0.01))],
+    }
     with open(OUT, "w") as f:
         json.dump(g, f, indent=0, sort_keys=True)
     print("wrote", OUT, os.path.getsize(OUT), "bytes")

@@ -143,3 +143,22 @@ def test_bench_single_layout_matches_witness(golden):
     r = benchmark.run_benchmark("ziggurat", "splitmix", benchmark.BenchConfig.single())
     assert r.ns_per_op > 0 and r.engine_used == "cuda"
     assert "%016x" % r.checksum == golden["bench_witness"]["splitmix/ziggurat/%d" % benchmark.DEFAULT_SEED]
+
+
+def test_bench_and_stats_host_helpers_match_reference(golden_cli):
+    from paper_2405_19493_b200 import benchmark, verify
+
+    h = golden_cli["host_fns"]
+    for c, d, v in h["t_quantile"]:
+        assert abs(benchmark.student_t_quantile(c, d) - float.fromhex(v)) <= 1e-12 * max(1.0, abs(float.fromhex(v)))
+    for xs, lvl, (lo, hi) in h["ci"]:
+        a, b = benchmark.confidence_interval(xs, lvl)
+        assert abs(a - float.fromhex(lo)) < 1e-12 and abs(b - float.fromhex(hi)) < 1e-12
+    for b, c, v in h["percent_faster"]:
+        assert benchmark.percent_faster(b, c) == float.fromhex(v)
+    for a, b, x, v in h["beta"]:
+        assert abs(verify.regularized_beta(a, b, x) - float.fromhex(v)) < 1e-14
+    with pytest.raises(ValueError):
+        benchmark.percent_faster(0.0, 1.0)
+    with pytest.raises(ValueError):
+        benchmark.confidence_interval([1.0], 0.9)

@@ -632,3 +632,16 @@ print(repr(res))
         assert r.returncode == 0, r.stderr[-2000:]
         outs.append(r.stdout.strip().splitlines()[-1])
     assert outs[0] == outs[1]
+
+
+@pytest.mark.parametrize("source", ["lcg48", "splitmix"])
+def test_tail_sample_matches_oracle(source):
+    for seed in range(20):
+        src = gz.make_source(source, seed)
+        st = engine._state_words(src)
+        r = 3.4426198558966377 if seed % 2 else 0.5
+        v = gz.tail_sample(src, r)
+        rv, rst, status = O.tail_sample(source, st, r)
+        assert status == 0 and v == rv and src.state == int(rst[0])
+    with pytest.raises(ValueError):
+        gz.tail_sample(gz.make_source(source, 1), 0.0)
