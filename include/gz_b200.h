@@ -12,6 +12,8 @@
  *   GZ_ERR_INVALID (2)  invalid argument (engine.py:209,269 TypeError /
  *                        tables.py:109-110 ValueError)
  *   GZ_ERR_CUDA (3)     CUDA runtime error (no device, launch failure, ...)
+ *   GZ_ERR_EXHAUSTED (4) a scripted source ran out of words (sources.py
+ *                       ScriptExhausted)
  *
  * gz_last_error() returns a message for the last non-zero status of the calling
  * thread.  "Device" pointers are CUDA device (or managed) memory of the current
@@ -38,6 +40,7 @@ extern "C" {
 #define GZ_ERR_GUARD 1
 #define GZ_ERR_INVALID 2
 #define GZ_ERR_CUDA 3
+#define GZ_ERR_EXHAUSTED 4
 
 /* samplers.py:225-237 SAMPLER_IDS */
 #define GZ_ALG_POLAR 0
@@ -203,6 +206,22 @@ int gz_polar_ops_selftest(int64_t n, uint64_t seed, uint64_t* counts2, void* cud
  * Guard trips are reported by gz_stream_check.
  */
 int gz_tail_sample(int src, uint64_t* state, double r, int64_t guard, double* out, void* cuda_stream);
+
+/*
+ * Deviates from a scripted source (sources.py ScriptedSource, the reference's test
+ * double): the sampler loop of samplers.py run by one device thread over the
+ * words[n_words] (device) from *cursor (device, advanced past the consumed
+ * words).  n deviates into out (device); polar spares as in gz_fill_gaussians
+ * (single values, device).  Reading past the last word reports GZ_ERR_EXHAUSTED
+ * through gz_stream_check.  For tests and per-call replay, not throughput.
+ */
+int gz_fill_scripted(int alg, int table_slot, const uint64_t* words, int64_t n_words, int64_t* cursor, int64_t n,
+                     double* out, const double* spare_in, const uint8_t* has_spare_in, double* spare_out,
+                     uint8_t* has_spare_out, int64_t guard, void* cuda_stream);
+
+/* gz_tail_sample over scripted words (words/cursor as in gz_fill_scripted). */
+int gz_tail_scripted(const uint64_t* words, int64_t n_words, int64_t* cursor, double r, int64_t guard, double* out,
+                     void* cuda_stream);
 
 /* xor-fold of u64[n] (device) into *out (device): the global checksum. */
 int gz_xor_reduce(const uint64_t* in, int64_t n, uint64_t* out, void* cuda_stream);

@@ -13,7 +13,7 @@ import threading
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("GZ_LIB") or os.path.join(HERE, "libgzb200.so")   # GZ_LIB: alternate build (experiments)
 
-GZ_OK, GZ_ERR_GUARD, GZ_ERR_INVALID, GZ_ERR_CUDA = 0, 1, 2, 3
+GZ_OK, GZ_ERR_GUARD, GZ_ERR_INVALID, GZ_ERR_CUDA, GZ_ERR_EXHAUSTED = 0, 1, 2, 3, 4
 ALG = {"polar": 0, "ziggurat": 1, "modified-ziggurat": 2}
 SRC = {"lcg48": 0, "splitmix": 1}
 SEED = {"lcg_master_plus_id": 0, "sm_output_of_master": 1, "sm_id_xor_master": 2, "sm_master_plus_id": 3}
@@ -24,7 +24,8 @@ EXPORTS = ("gz_version", "gz_last_error", "gz_device_count", "gz_set_kernel_poli
            "gz_fill_unit_affine", "gz_mutate", "gz_moments_reduce", "gz_xor_reduce", "gz_stream_check",
            "gz_host_alloc", "gz_host_free", "gz_build_tables", "gz_hist_edges", "gz_ks_stat", "gz_lowbits_hist", "gz_libm_eval_device", "gz_libm_exp",
            "gz_libm_log", "gz_moments_buffer", "gz_zig_occupancy",
-           "gz_wedge_filter_error", "gz_polar_ops_selftest", "gz_tail_sample")
+           "gz_wedge_filter_error", "gz_polar_ops_selftest", "gz_tail_sample", "gz_fill_scripted",
+           "gz_tail_scripted")
 
 
 class EngineUnavailable(RuntimeError):
@@ -77,6 +78,8 @@ def load(require_device: bool = True):
             L.gz_wedge_filter_error.argtypes = [I, i64, ctypes.c_uint64, P, P]
             L.gz_polar_ops_selftest.argtypes = [i64, ctypes.c_uint64, P, P]
             L.gz_tail_sample.argtypes = [I, P, D, i64, P, P]
+            L.gz_fill_scripted.argtypes = [I, I, P, i64, P, i64, P, P, P, P, P, i64, P]
+            L.gz_tail_scripted.argtypes = [P, i64, P, D, i64, P, P]
             L.gz_libm_exp.argtypes = [D]
             L.gz_libm_exp.restype = D
             L.gz_libm_log.argtypes = [D]
@@ -96,4 +99,8 @@ def check(status: int) -> None:
         raise RejectionLoopExceeded(msg)
     if status == GZ_ERR_INVALID:
         raise ValueError(msg)
+    if status == GZ_ERR_EXHAUSTED:
+        from .sources import ScriptExhausted
+
+        raise ScriptExhausted(msg)
     raise RuntimeError(f"CUDA error: {msg}")

@@ -302,3 +302,133 @@ __global__ void k_tail_sample(uint64_t* state, double r, int64_t guard, double* 
     out[0] = to.v;
 }
 
+/* ------------------------------------------------------ scripted sources */
+
+/* a scripted word stream on the device: words[cursor++], exhaustion flagged */
+struct ScriptDraws {
+    const uint64_t* w;
+    int64_t n, pos;
+    bool out;   /* read past the end */
+    __device__ __forceinline__ uint64_t next()
+    {
+        if (pos >= n) {
+            out = true;
+            return 0;
+        }
+        return w[pos++];
+    }
+    __device__ __forceinline__ double unit() { return gz_unit53(next()); }
+};
+
+/* samplers.py:95-115 / 144-165 (ziggurats) and 179-192 (polar), call after call,
+   over scripted words, by one thread */
+__global__ void k_scripted(int alg, const ulonglong2* kw, const double2* yd, int n_layers, double r,
+                           const uint64_t* words, int64_t n_words, int64_t* cursor, int64_t n, double* out,
+                           const double* spare_in, const uint8_t* has_in, double* spare_out, uint8_t* has_out,
+                           int64_t guard)
+{
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    ScriptDraws d{words, n_words, *cursor, false};
+    int ib = 0;
+    while (alg != GZ_ALG_POLAR && alg != 3 && (1 << (ib + 1)) <= n_layers) ++ib;
+    const uint32_t imask = (uint32_t)n_layers - 1u;
+    const int mbits = 63 - ib;
+    const uint64_t mmask = (alg == 1 || alg == 2) ? (1ULL << mbits) - 1ULL : 0;
+    bool has = alg == GZ_ALG_POLAR && has_in && has_in[0];
+    double spare = has ? spare_in[0] : 0.0;
+    int code = 0;
+    for (int64_t c = 0; c < n && !code; ++c) {
+        double v = 0.0;
+        bool done = false;
+        if (alg == 3) {
+            /* tail_sample(src, r) calls (samplers.py:40-57) */
+            for (int64_t t = 0; t < guard && !done; ++t) {
+                const double u1 = d.unit(), u2 = d.unit();
+                if (d.out) break;
+                if (u1 <= 0.0 || u2 <= 0.0) continue;
+                const double xt = __ddiv_rn(-gz_log_t(u1, g_log_tab), r);
+                const double yt = -gz_log_t(u2, g_log_tab);
+                if (__dmul_rn(2.0, yt) > __dmul_rn(xt, xt)) {
+                    v = __dadd_rn(r, xt);
+                    done = true;
+                }
+            }
+        } else if (alg == GZ_ALG_POLAR) {
+            if (has) {
+                has = false;
+                v = spare;
+                done = true;
+            }
+            for (int64_t a = 0; a < guard && !done; ++a) {
+                const double v1 = __fma_rn(2.0, d.unit(), -1.0);
+                const double v2 = __fma_rn(2.0, d.unit(), -1.0);
+                if (d.out) break;
+                const double s = __dadd_rn(__dmul_rn(v1, v1), __dmul_rn(v2, v2));
+                if (s > 0.0 && s < 1.0) {
+                    const double mul = polar_mul(s, g_log_tab);
+                    v = __dmul_rn(v1, mul);
+                    spare = __dmul_rn(v2, mul);
+                    has = true;
+                    done = true;
+                }
+            }
+        } else {
+            const bool mod = alg == GZ_ALG_MODIFIED_ZIGGURAT;
+            for (int64_t a = 0; a < guard && !done; ++a) {
+                const uint64_t u = d.next();
+                if (d.out) break;
+                uint32_t i;
+                uint64_t m;
+                bool neg;
+                if (mod) {
+                    i = (uint32_t)u & imask;
+                    m = u >> (ib + 1);
+                    neg = (u >> ib) & 1;
+                } else {
+                    i = (uint32_t)(u >> mbits) & imask;
+                    m = u & mmask;
+                    neg = u >> 63;
+                }
+                const ulonglong2 k = kw[i];
+                double x = __dmul_rn(__ull2double_rn(m), __longlong_as_double((long long)k.y));
+                bool ok = m < k.x;
+                if (!ok && i == 0) {
+                    /* tail_sample (samplers.py:40-57) */
+                    for (int64_t t = 0; t < guard && !ok; ++t) {
+                        const double u1 = d.unit(), u2 = d.unit();
+                        if (d.out) break;
+                        if (u1 <= 0.0 || u2 <= 0.0) continue;
+                        const double xt = __ddiv_rn(-gz_log_t(u1, g_log_tab), r);
+                        const double yt = -gz_log_t(u2, g_log_tab);
+                        if (__dmul_rn(2.0, yt) > __dmul_rn(xt, xt)) {
+                            x = __dadd_rn(r, xt);
+                            ok = true;
+                        }
+                    }
+                    if (!ok && !d.out) {
+                        code = GZ_ERR_GUARD;
+                        break;
+                    }
+                } else if (!ok) {
+                    const double y = __dadd_rn(yd[i].x, __dmul_rn(d.unit(), yd[i].y));
+                    if (d.out) break;
+                    ok = wedge_exact(y, __dmul_rn(__dmul_rn(-0.5, x), x));
+                }
+                if (ok) {
+                    v = neg ? -x : x;
+                    done = true;
+                }
+            }
+        }
+        if (d.out) code = GZ_ERR_EXHAUSTED;
+        else if (!done && !code) code = GZ_ERR_GUARD;
+        if (!code) out[c] = v;
+    }
+    if (code) gz_raise(code, 0);
+    *cursor = d.pos;
+    if (alg == GZ_ALG_POLAR) {
+        if (spare_out) spare_out[0] = has ? spare : 0.0;
+        if (has_out) has_out[0] = has ? 1 : 0;
+    }
+}
+

@@ -25,7 +25,7 @@ import numpy as np
 from . import _lib
 from ._lib import DEFAULT_GUARD, EngineUnavailable, RejectionLoopExceeded, check
 from .samplers import GaussianSampler, ModifiedZigguratSampler, PolarSampler, ZigguratSampler
-from .sources import Lcg48, SplitMix64, UniformSource, make_source
+from .sources import Lcg48, ScriptedSource, ScriptExhausted, SplitMix64, UniformSource, make_source
 from .tables import ZigguratTables
 
 __all__ = ["available", "supports", "fill_u64", "fill_gaussians", "warm_up", "table_slot", "EngineUnavailable",
@@ -46,8 +46,43 @@ def available() -> bool:
 
 
 def supports(source: UniformSource) -> bool:
-    """Whether a device kernel exists for this source (engine.py:199-201)."""
-    return isinstance(source, (Lcg48, SplitMix64)) and available()
+    """Whether a device kernel exists for this source (engine.py:199-201): the two
+    PRNGs, and the scripted test double (replayed call by call by one device thread)."""
+    return isinstance(source, (Lcg48, SplitMix64, ScriptedSource)) and available()
+
+
+def _fill_scripted(sampler: GaussianSampler, source: ScriptedSource, out, guard: int) -> None:
+    """Scripted words replayed on the device (gz_fill_scripted): the sampler loop of
+    samplers.py by one thread; the source's cursor and the polar spare advance like
+    the reference's per-call path."""
+    import torch
+
+    L = _lib.load()
+    alg = _alg_of(sampler)
+    slot = 0 if alg == 0 else table_slot(sampler.tables)
+    n = len(out)
+    words = np.array(source.words[source.cursor:], dtype=np.uint64)
+    d_w = torch.from_numpy(words.view(np.int64).copy()).to("cuda")
+    d_c = torch.zeros(1, dtype=torch.int64, device="cuda")
+    d_out = out if _is_cuda_tensor(out) else torch.empty(n, dtype=torch.float64, device="cuda")
+    polar = alg == 0
+    sp = torch.tensor([sampler.spare if polar and sampler.spare is not None else 0.0], dtype=torch.float64,
+                      device="cuda")
+    hs = torch.tensor([1 if polar and sampler.spare is not None else 0], dtype=torch.uint8, device="cuda")
+    spo = torch.zeros(1, dtype=torch.float64, device="cuda")
+    hso = torch.zeros(1, dtype=torch.uint8, device="cuda")
+    s = torch.cuda.current_stream().cuda_stream
+    check(L.gz_fill_scripted(alg, slot, _ptr(d_w), words.size, _ptr(d_c), n, _ptr(d_out),
+                             _ptr(sp) if polar else None, _ptr(hs) if polar else None,
+                             _ptr(spo) if polar else None, _ptr(hso) if polar else None, guard, s))
+    try:
+        check(L.gz_stream_check(s))
+    finally:
+        source.cursor += int(d_c.cpu()[0])
+    if not _is_cuda_tensor(out):
+        out[...] = d_out.cpu().numpy()
+    if polar:
+        sampler.spare = float(spo.cpu()[0]) if int(hso.cpu()[0]) else None
 
 
 # ---- table slots --------------------------------------------------------------
@@ -132,6 +167,20 @@ def _is_cuda_tensor(out) -> bool:
 
 def fill_u64(source: UniformSource, out) -> None:
     """Fill `out` (uint64, 1-D) with draws, advancing the source in place."""
+    if isinstance(source, ScriptedSource):
+        n = len(out)
+        if source.remaining() < n:
+            source.cursor = len(source.words)
+            raise ScriptExhausted(f"script exhausted after {len(source.words)} words")
+        words = np.array(source.words[source.cursor:source.cursor + n], dtype=np.uint64)
+        source.cursor += n
+        if _is_cuda_tensor(out):
+            import torch
+
+            out.copy_(torch.from_numpy(words.view(np.int64)))
+        else:
+            np.asarray(out).view(np.uint64)[...] = words
+        return
     L = _lib.load()
     st = _state_words(source)
     src = _lib.SRC[source.source_id]
@@ -166,6 +215,9 @@ def fill_u64(source: UniformSource, out) -> None:
 def fill_gaussians(sampler: GaussianSampler, source: UniformSource, out, guard: int = DEFAULT_GUARD) -> None:
     """Fill `out` (float64, 1-D) with deviates, advancing sampler and source
     state exactly as `sampler.next_gaussian(source)` called len(out) times would."""
+    if isinstance(source, ScriptedSource):
+        _alg_of(sampler)
+        return _fill_scripted(sampler, source, out, guard)
     L = _lib.load()
     alg = _alg_of(sampler)
     st = _state_words(source)

@@ -36,6 +36,21 @@ def tail_sample(src, r: float, guard: int = LOOP_GUARD) -> float:
     if not r > 0.0:
         raise ValueError(f"tail boundary must be positive, got {r}")
     L = load()
+    from .sources import ScriptedSource
+
+    if isinstance(src, ScriptedSource):
+        words = np.array(src.words[src.cursor:], dtype=np.uint64)
+        d_w = torch.from_numpy(words.view(np.int64).copy()).to("cuda")
+        d_c = torch.zeros(1, dtype=torch.int64, device="cuda")
+        out = torch.zeros(1, dtype=torch.float64, device="cuda")
+        s = torch.cuda.current_stream().cuda_stream
+        check(L.gz_tail_scripted(ctypes.c_void_p(d_w.data_ptr()), words.size, ctypes.c_void_p(d_c.data_ptr()),
+                                 float(r), guard, ctypes.c_void_p(out.data_ptr()), s))
+        try:
+            check(L.gz_stream_check(s))
+        finally:
+            src.cursor += int(d_c.cpu()[0])
+        return float(out.cpu()[0])
     st = engine._state_words(src)
     d = torch.from_numpy(st.view(np.int64).copy()).to("cuda")
     out = torch.zeros(1, dtype=torch.float64, device="cuda")

@@ -123,12 +123,35 @@ def test_fill_u64_matches_reference(source, golden):
     assert "%016x" % src.state == g["state"]
 
 
-def test_scripted_source_is_refused():
-    smp = gz.make_sampler("ziggurat")
-    assert not engine.supports(gz.ScriptedSource([1, 2, 3]))
-    assert engine.supports(gz.make_source("lcg48", 0)) and engine.supports(gz.make_source("splitmix", 0))
-    with pytest.raises(TypeError):
-        engine.fill_gaussians(smp, gz.ScriptedSource([1, 2, 3]), np.empty(4))
+def test_scripted_sources_replay_like_the_reference(golden_cli):
+    """Scripted words (the reference's test double) replayed on the device call by call:
+    fast path, sign flip, tail, wedge accept/reject, the modified layout, polar with
+    spares, and exhaustion -- values, cursor and spare equal the reference's."""
+    assert engine.supports(gz.ScriptedSource([1, 2, 3]))
+    for r in golden_cli["scripted"]:
+        smp = gz.make_sampler(r["sampler"])
+        if r["spare_in"] is not None:
+            smp.spare = r["spare_in"]
+        src = gz.ScriptedSource([int(w, 16) for w in r["words"]])
+        vals = []
+        if r["exhausted"]:
+            with pytest.raises(gz.ScriptExhausted):
+                for _ in range(r["n"]):
+                    vals.append(smp.next_gaussian(src).hex())
+        else:
+            buf = np.empty(r["n"])
+            engine.fill_gaussians(smp, src, buf)
+            vals = [float(v).hex() for v in buf]
+        assert vals == r["values"], r["sampler"]
+        assert src.cursor == r["cursor"]
+        if not r["exhausted"]:
+            assert (None if smp.__dict__.get("spare") is None else smp.spare.hex()) == r["spare_out"]
+
+
+def test_tail_sample_scripted_matches_reference(golden_cli):
+    for rr, words, v in golden_cli["tail"]:
+        src = gz.ScriptedSource([int(w, 16) for w in words])
+        assert gz.tail_sample(src, rr).hex() == v
 
 
 # ---- multi-stream hot path ------------------------------------------------------
