@@ -537,8 +537,9 @@ def test_single_long_stream_vs_oracle(source, alg, n):
         st_np = rng.integers(0, 2 ** 63, size=(1, 2), dtype=np.uint64) * np.uint64(2) + np.uint64(1)
     kw, sp, hs = {}, None, None
     if alg == "polar":
-        hs = np.array([n % 2], dtype=np.uint8)
-        sp = np.array([0.25 * (n % 2)])
+        has = 1 if n in (32768, 100001) else 0     # spare in with an odd and an even remainder
+        hs = np.array([has], dtype=np.uint8)
+        sp = np.array([0.25 * has])
         kw = dict(spare=torch.from_numpy(sp.copy()).to(DEV), has_spare=torch.from_numpy(hs.copy()).to(DEV))
     st = dev_states(source, st_np)
     out = torch.empty((1, n), dtype=torch.float64, device=DEV)
@@ -607,7 +608,7 @@ def test_fill_u64_single_long_stream(source, n):
     assert src.state == int(ref_st.reshape(-1)[0])
 
 
-@pytest.mark.parametrize("n", [40001, 65536])
+@pytest.mark.parametrize("n", [40001, 65536, 65537])
 def test_polar_single_stream_host_path_with_spare(n):
     """numpy output, cached spare in and out, one long stream (gz_fill_gaussians_host ->
     the whole-GPU decode) against the per-call oracle semantics."""

@@ -1,0 +1,106 @@
+"""Randomised parity sweep of the CUDA engine against the CPU oracle (test tool).
+
+    python tools/fuzz_gpu.py SECONDS [SEED]
+
+Random pairing, stream count, row length, states, polar spares, kernel policy and
+device or host (numpy, gz_fill_gaussians_host) buffers per case; every output, final state and spare must equal the oracle's bit for bit.
+Prints one line per 50 cases and a final summary; exits 1 on the first mismatch.
+"""
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+from oracle import gz_oracle as O
+from paper_2405_19493_b200 import _lib, streams
+from paper_2405_19493_b200.engine import table_slot
+from paper_2405_19493_b200.samplers import make_sampler
+
+PAIRINGS = [(s, a) for s in ("lcg48", "splitmix") for a in ("polar", "ziggurat", "modified-ziggurat")]
+
+
+def one_case(rng):
+    source, alg = PAIRINGS[rng.integers(len(PAIRINGS))]
+    shape = rng.integers(4)
+    if shape == 0:
+        n, n_per = 1, int(rng.integers(32768, 300000))          # whole-GPU single-stream decode
+    elif shape == 1:
+        n, n_per = int(rng.integers(1, 200)), int(rng.integers(0, 3000))
+    elif shape == 2:
+        n, n_per = int(rng.integers(32768, 45000)), int(rng.integers(1, 80))
+    else:
+        n, n_per = int(rng.integers(200, 3000)), int(rng.integers(0, 600))
+    policy = ["auto", "warp", "lane"][rng.integers(3)]
+    raw = rng.integers(0, 2 ** 63, size=(n, 2), dtype=np.uint64) * np.uint64(2) + rng.integers(0, 2, size=(n, 2),
+                                                                                               dtype=np.uint64)
+    st_np = raw[:, 0] & np.uint64((1 << 48) - 1) if source == "lcg48" else raw.copy()
+    if source == "splitmix":
+        st_np[:, 1] |= np.uint64(1)
+    kw, sp, hs = {}, None, None
+    if alg == "polar":
+        hs = rng.integers(0, 2, size=n).astype(np.uint8)
+        sp = rng.standard_normal(n) * hs
+        kw = dict(spare=torch.from_numpy(sp.copy()).cuda(), has_spare=torch.from_numpy(hs.copy()).cuda())
+    host = bool(rng.integers(2))      # host buffers through gz_fill_gaussians_host
+    streams.set_kernel_policy(policy)
+    try:
+        if host:
+            L = _lib.load()
+            a = {"polar": 0, "ziggurat": 1, "modified-ziggurat": 2}[alg]
+            slot = table_slot(make_sampler(alg).tables) if a else 0
+            st_in = np.ascontiguousarray(st_np)
+            st_h = np.empty_like(st_in)
+            out_h = np.empty((n, n_per))
+            sp_o, hs_o = np.zeros(n), np.zeros(n, dtype=np.uint8)
+            pp = lambda x: x.ctypes.data if x is not None else None
+            _lib.check(L.gz_fill_gaussians_host(a, _lib.SRC[source], slot, n, n_per, pp(st_in), pp(st_h),
+                                                pp(sp) if a == 0 else None, pp(hs) if a == 0 else None,
+                                                pp(sp_o) if a == 0 else None, pp(hs_o) if a == 0 else None,
+                                                pp(out_h), None, 1_000_000))
+            got, got_st = out_h, st_h.reshape(-1)
+            if a == 0:
+                kw = dict(spare=torch.from_numpy(sp_o), has_spare=torch.from_numpy(hs_o))
+        else:
+            st = torch.from_numpy(np.ascontiguousarray(st_np).view(np.int64).copy()).cuda()
+            out = torch.empty((n, n_per), dtype=torch.float64, device="cuda")
+            streams.fill_gaussians_streams(alg, source, st, out, **kw)
+            got, got_st = out.cpu().numpy(), st.cpu().numpy().view(np.uint64)
+    finally:
+        streams.set_kernel_policy("auto")
+    ref, ref_st, ref_sp, ref_has, status = O.fill_gaussians(alg, source, st_np, n_per,
+                                                             *((sp, hs) if alg == "polar" else (None, None)))
+    desc = f"{source}/{alg} n={n} n_per={n_per} policy={policy} host={host}"
+    assert status == 0, desc
+    assert np.array_equal(got.view(np.uint64), ref.view(np.uint64)), "values " + desc
+    assert np.array_equal(got_st.reshape(ref_st.shape), ref_st), "state " + desc
+    if alg == "polar":
+        h = kw["has_spare"].cpu().numpy()
+        assert np.array_equal(h, ref_has), "has " + desc
+        assert np.array_equal((kw["spare"].cpu().numpy() * h).view(np.uint64), (ref_sp * ref_has).view(np.uint64)), \
+            "spare " + desc
+    return n * n_per
+
+
+def main():
+    secs = float(sys.argv[1]) if len(sys.argv) > 1 else 60.0
+    rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 12345)
+    t_end = time.time() + secs
+    cases = total = 0
+    while time.time() < t_end:
+        try:
+            total += one_case(rng)
+        except AssertionError as e:
+            print("MISMATCH", e, flush=True)
+            return 1
+        cases += 1
+        if cases % 50 == 0:
+            print(f"{cases} cases, {total} deviates ok", flush=True)
+    print(f"fuzz ok: {cases} cases, {total} deviates, all bit-exact", flush=True)
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())
