@@ -3,7 +3,8 @@
     python tools/fuzz_gpu.py SECONDS [SEED]
 
 Random pairing, stream count, row length, states, polar spares, kernel policy and
-device or host (numpy, gz_fill_gaussians_host) buffers per case; every output, final state and spare must equal the oracle's bit for bit.
+device or host (numpy, gz_fill_gaussians_host) buffers per case, plus random
+mutate (config-5) and fill_u64 cases; every output, final state and spare must equal the oracle's bit for bit.
 Prints one line per 50 cases and a final summary; exits 1 on the first mismatch.
 """
 import os
@@ -84,6 +85,48 @@ def one_case(rng):
     return n * n_per
 
 
+def mutate_case(rng):
+    n, genes, gens = int(rng.integers(1, 3000)), int(rng.integers(1, 700)), int(rng.integers(1, 4))
+    pad = int(rng.integers(0, 3))
+    policy = ["auto", "warp", "lane"][rng.integers(3)]
+    st_np = rng.integers(0, 2 ** 63, size=(n, 2), dtype=np.uint64)
+    st_np[:, 1] |= np.uint64(1)
+    x_np = rng.standard_normal((n, genes))
+    sig = np.abs(rng.standard_normal(n)) * (rng.random(n) < 0.9)
+    full = torch.zeros((n, genes + pad), dtype=torch.float64, device="cuda")
+    full[:, :genes] = torch.from_numpy(x_np)
+    x = full[:, :genes]
+    st = torch.from_numpy(st_np.view(np.int64).copy()).cuda()
+    streams.set_kernel_policy(policy)
+    try:
+        streams.mutate(st, x, torch.from_numpy(sig).cuda(), gens)
+    finally:
+        streams.set_kernel_policy("auto")
+    xr = x_np.copy()
+    ref_st, status = O.mutate(st_np, xr, sig, gens)
+    desc = f"mutate n={n} genes={genes} gens={gens} pad={pad} policy={policy}"
+    assert status == 0, desc
+    assert np.array_equal(x.cpu().numpy().view(np.uint64), xr.view(np.uint64)), "values " + desc
+    assert np.array_equal(st.cpu().numpy().view(np.uint64), ref_st), "state " + desc
+    return n * genes * gens
+
+
+def u64_case(rng):
+    source = ["lcg48", "splitmix"][rng.integers(2)]
+    n, n_per = (1, int(rng.integers(1, 400000))) if rng.integers(2) else (int(rng.integers(1, 5000)),
+                                                                          int(rng.integers(0, 300)))
+    st_np = rng.integers(0, 2 ** 48, size=n, dtype=np.uint64) if source == "lcg48" else \
+        rng.integers(0, 2 ** 63, size=(n, 2), dtype=np.uint64) | np.uint64(1)
+    st = torch.from_numpy(np.ascontiguousarray(st_np).view(np.int64).copy()).cuda()
+    out = torch.empty((n, n_per), dtype=torch.int64, device="cuda")
+    streams.fill_u64_streams(source, st, out)
+    ref, ref_st = O.fill_u64(source, st_np, n_per)
+    desc = f"u64 {source} n={n} n_per={n_per}"
+    assert np.array_equal(out.cpu().numpy().view(np.uint64), ref), "values " + desc
+    assert np.array_equal(st.cpu().numpy().view(np.uint64).reshape(ref_st.shape), ref_st), "state " + desc
+    return n * n_per
+
+
 def main():
     secs = float(sys.argv[1]) if len(sys.argv) > 1 else 60.0
     rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 12345)
@@ -91,7 +134,8 @@ def main():
     cases = total = 0
     while time.time() < t_end:
         try:
-            total += one_case(rng)
+            k = rng.random()
+            total += (one_case if k < 0.7 else mutate_case if k < 0.9 else u64_case)(rng)
         except AssertionError as e:
             print("MISMATCH", e, flush=True)
             return 1
