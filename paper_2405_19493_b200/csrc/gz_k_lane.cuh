@@ -248,6 +248,24 @@ __device__ __forceinline__ void sts_f64(uint32_t a, double v)
     asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
 }
 
+/* lane_stats over a full group: cnt == LK and f a multiple of LK, so the LK values
+   are contiguous in the ring (same order, same roundings as lane_stats) */
+__device__ __forceinline__ void lane_stats_full(uint32_t myring_sh, int f, uint64_t& ck, double& a1, double& a2,
+                                                double& a3, double& a4)
+{
+    const uint32_t base = myring_sh + 8 * (f & (LRING - 1));
+#pragma unroll
+    for (int c = 0; c < LK; ++c) {
+        const double v = lds_f64(base + 8 * c);
+        ck ^= (uint64_t)__double_as_longlong(v);
+        const double v2 = __dmul_rn(v, v);
+        a1 = __dadd_rn(a1, v);
+        a2 = __dadd_rn(a2, v2);
+        a3 = __fma_rn(v2, v, a3);
+        a4 = __fma_rn(v2, v2, a4);
+    }
+}
+
 template <int SRC, int IBT, bool MOD, bool STATS, int EPI = EPI_STORE>
 __global__ void __launch_bounds__(LANE_THREADS, EPI == EPI_MUTATE ? 2 : 3) k_zig_lane(const __grid_constant__ LaneParams p)
 {
@@ -382,7 +400,10 @@ __global__ void __launch_bounds__(LANE_THREADS, EPI == EPI_MUTATE ? 2 : 3) k_zig
             const int cnt = lag >= LK ? LK : (done ? total - flushed : 0);
             if (cnt > 0) {
                 __syncwarp();
-                if constexpr (STATS) lane_stats(myring, flushed, cnt, ck, a1, a2, a3, a4);
+                if constexpr (STATS) {
+                    if (cnt == LK) lane_stats_full(myring_sh, flushed, ck, a1, a2, a3, a4);
+                    else lane_stats(myring, flushed, cnt, ck, a1, a2, a3, a4);
+                }
                 lane_flush(ring, p.out, p.ld, row0, n_streams, flushed, fcol, cnt, p.vec_ok, lane);
                 flushed += cnt;
                 if constexpr (EPI == EPI_MUTATE) {
