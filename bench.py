@@ -204,6 +204,35 @@ def time_mutate(first_ind, n_ind, generations, steps, warmup, world):
             "launches": steps}
 
 
+# the polar x LCG48 path is bounded by HBM stores (8 B/variate), the
+# integer pipe and (for polar) the FP64 pipe.  Algorithmic operations per variate:
+#   int : 1.2725 u64/variate x ~10 SASS int ops per LCG48 u64 (2 x mul-add + shifts)
+#         + ~10 for extraction / compare / conversion                      = 22.7
+#   fp64: per attempt (0.6363/variate) 2 x (int->f64, 2u-1) + s (3) + 2 compares = 9;
+#         per pair (0.5/variate) glibc log table path 15, -2*log 1, divide 8,
+#         square root 9, the two products 2                                 = 35
+#         -> 0.6363 * 9 + 0.5 * 35                                          = 23.2
+# Pipe rates per SM per clock: int32 64 (CUDA throughput table, cc 10.0); FP64 62
+# (measured, tools/calib/calib_pipes.cu).  Clock: the median sampled under load.
+INT_OPS_PER_VARIATE = 22.7
+FP64_OPS_PER_VARIATE = 23.2
+INT_OPS_PER_SM_CLK = 64
+FP64_OPS_PER_SM_CLK = 62
+
+
+def compute_bounds(variates_per_s, hbm_gbs, clocks):
+    import torch
+
+    sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    mhz = (clocks or {}).get("sm_mhz") or 1965.0
+    hz = mhz * 1e6
+    b = {"hbm": hbm_gbs * 1e9 / 8, "int": sms * hz * INT_OPS_PER_SM_CLK / INT_OPS_PER_VARIATE,
+         "fp64": sms * hz * FP64_OPS_PER_SM_CLK / FP64_OPS_PER_VARIATE}
+    lim = min(b, key=b.get)
+    return {"unit": "variates/s", "sm_mhz": mhz, "sms": sms, **b, "min": lim,
+            "frac_of_min": variates_per_s / b[lim]}
+
+
 def e2e_host(first_id, n_streams, steps, warmup):
     """Reference-facing path: host buffers through gz_fill_gaussians_host."""
     import ctypes
@@ -373,7 +402,9 @@ def main():
                        "l2": "output 2 GiB per step > 126 MB L2 (no flush needed)", "parallelism": f"streams/{world}"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak, "traffic": tr, "peak_kind": peak_kind,
-                         "algorithmic_bytes_per_launch": kernel_bytes},
+                         "algorithmic_bytes_per_launch": kernel_bytes,
+                         "compute_bounds": compute_bounds(r["variates_per_step"] / (r["ms_per_step"] / 1e3),
+                                                          hbm_peak, clocks)},
             "e2e": e2e, "gpu_launches": launches, "clocks": clocks, "configs": extra,
         }
         if cpu is not None:
