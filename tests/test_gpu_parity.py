@@ -669,3 +669,51 @@ def test_tail_sample_matches_oracle(source):
         assert status == 0 and v == rv and src.state == int(rst[0])
     with pytest.raises(ValueError):
         gz.tail_sample(gz.make_source(source, 1), 0.0)
+
+
+def test_abi_rejects_bad_arguments_and_recovers():
+    """Every invalid call returns GZ_ERR_INVALID (2) with a message and launches
+    nothing; the next valid call works (no sticky error state)."""
+    from paper_2405_19493_b200 import _lib
+
+    L = _lib.load()
+    s = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    st = torch.zeros(8, 2, dtype=torch.int64, device=DEV)
+    out = torch.zeros(8, 16, dtype=torch.float64, device=DEV)
+    x = torch.zeros(8, 16, dtype=torch.float64, device=DEV)
+    sig = torch.ones(8, dtype=torch.float64, device=DEV)
+    sp = torch.zeros(8, dtype=torch.float64, device=DEV)
+    P = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
+    slot = engine.table_slot(gz.make_sampler("ziggurat").tables)
+    G = 1_000_000
+
+    def fill(alg=1, src=1, sl=slot, n=8, n_per=16, ld=16, si=True, so=True, o=True, spi=None, hi=None, guard=G):
+        return L.gz_fill_gaussians(alg, src, sl, n, n_per, ld, P(st) if si else None, P(st) if so else None,
+                                   spi, hi, None, None, P(out) if o else None, None, None, guard, s)
+
+    bad = {
+        "alg": fill(alg=3), "alg-neg": fill(alg=-1), "src": fill(src=2), "n": fill(n=-1), "n_per": fill(n_per=-1),
+        "ld": fill(ld=15), "guard": fill(guard=0), "state_in": fill(si=False), "state_out": fill(so=False),
+        "out": fill(o=False), "slot": fill(sl=63), "slot-neg": fill(sl=-1),
+        "spare-without-flag": fill(alg=0, spi=P(sp)),
+        "polar-row-limit": fill(alg=0, n=1, n_per=1 << 30, ld=1 << 30),
+        "u64-src": L.gz_fill_u64(5, 8, 16, 16, P(st), P(st), P(out), s),
+        "u64-ld": L.gz_fill_u64(1, 8, 16, 8, P(st), P(st), P(out), s),
+        "mutate-slot": L.gz_mutate(63, 8, 16, 16, P(st), P(st), P(x), P(sig), 1, G, s),
+        "mutate-ld": L.gz_mutate(slot, 8, 16, 8, P(st), P(st), P(x), P(sig), 1, G, s),
+        "mutate-gens": L.gz_mutate(slot, 8, 16, 16, P(st), P(st), P(x), P(sig), -1, G, s),
+        "seed-scheme": L.gz_seed_streams(99, 1, 0, 8, P(st), s),
+    }
+    for name, status in bad.items():
+        assert status == 2, (name, status)
+        assert L.gz_last_error().decode(), name
+    assert (out == 0).all() and (x == 0).all()
+    # nothing sticky: a valid call right after succeeds and matches the oracle
+    st_np = O.config_states("c1", range(8))
+    st.copy_(torch.from_numpy(st_np.view(np.int64)))
+    assert fill() == 0
+    _lib.check(L.gz_stream_check(s))
+    ref, *_ = O.fill_gaussians("ziggurat", "splitmix", st_np, 16)
+    assert bits_equal(out.cpu().numpy(), ref)
+    # n_streams == 0 and n_per == 0 are valid no-ops
+    assert fill(n=0) == 0 and fill(n_per=0, ld=0) == 0
