@@ -275,6 +275,8 @@ __global__ void __launch_bounds__(256) k_zig(const ZigParams p)
                     }
                     em[d] |= gz_bitrange(b, nF);
                     cnt += nF;
+                    /* the guard counts the rejections of one call: a fast-path deviate ends it */
+                    if (nF > 0) rej_run = 0;
                     if (f == 32) {
                         q = 32 * (d + 1);
                         break;

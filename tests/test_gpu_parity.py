@@ -381,6 +381,36 @@ def test_guard_exact_for_each_stream(policy):
         assert got == status, sid
 
 
+@pytest.mark.parametrize("alg,source", [("ziggurat", "splitmix"), ("ziggurat", "lcg48"),
+                                        ("modified-ziggurat", "splitmix")])
+@pytest.mark.parametrize("guard", [2, 3])
+def test_zig_guard_counts_per_call(alg, source, guard, policy):
+    """The ziggurat guard counts consecutive rejected attempts of ONE call
+    (samplers.py:95-115): any accepted deviate, fast path included, resets it.
+    Per stream, the device trips exactly when the oracle does, and the streams
+    that do not trip match it bit for bit."""
+    n, n_per = 96, 700
+    cfg = "c4" if source == "lcg48" else "c1"
+    st_np = O.config_states(cfg, range(n))
+    trips = 0
+    for sid in range(n):
+        one = st_np[sid:sid + 1]
+        ref, ref_st, *_, status = O.fill_gaussians(alg, source, one, n_per, guard=guard)
+        out = torch.empty((1, n_per), dtype=torch.float64, device=DEV)
+        st = dev_states(source, one)
+        try:
+            streams.fill_gaussians_streams(alg, source, st, out, guard=guard)
+            got = 0
+        except gz.RejectionLoopExceeded:
+            got = 1
+        assert got == status, (sid, got, status)
+        trips += status
+        if not status:
+            assert bits_equal(out.cpu().numpy(), ref) and np.array_equal(u64(st).reshape(ref_st.shape), ref_st)
+    if guard == 2:
+        assert 0 < trips < n    # distinguishes per-call from cumulative counting
+
+
 @pytest.mark.parametrize("fn", [0, 1])
 def test_device_libm_bit_exact_sweep(fn):
     """The kernels' exp/log restatement equals the host glibc bit for bit."""
