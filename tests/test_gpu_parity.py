@@ -747,3 +747,59 @@ def test_abi_rejects_bad_arguments_and_recovers():
     assert bits_equal(out.cpu().numpy(), ref)
     # n_streams == 0 and n_per == 0 are valid no-ops
     assert fill(n=0) == 0 and fill(n_per=0, ld=0) == 0
+
+
+@pytest.mark.parametrize("source,alg", [("splitmix", "ziggurat"), ("lcg48", "ziggurat"),
+                                        ("splitmix", "modified-ziggurat"), ("lcg48", "modified-ziggurat")])
+def test_few_long_streams_segmented_vs_oracle(source, alg):
+    """Fewer streams than the GPU holds warps: G warps per stream decode speculative
+    segments (gz_k_seg.cuh) -- values and final states equal the oracle's for row
+    lengths around the segment sizes and stream counts up to one wave."""
+    for n, n_per in ((1, 512), (1, 20000), (2, 700), (7, 4096), (300, 513), (1024, 4096), (1100, 600)):
+        rng = np.random.default_rng(zlib.crc32(f"seg/{source}/{alg}/{n}/{n_per}".encode()))
+        if source == "lcg48":
+            st_np = rng.integers(0, 2 ** 48, size=n, dtype=np.uint64)
+        else:
+            st_np = rng.integers(0, 2 ** 63, size=(n, 2), dtype=np.uint64) | np.uint64(1)
+        st = dev_states(source, st_np)
+        out = torch.empty((n, n_per), dtype=torch.float64, device=DEV)
+        streams.fill_gaussians_streams(alg, source, st, out)
+        ref, ref_st, *_ = O.fill_gaussians(alg, source, st_np, n_per)
+        assert bits_equal(out.cpu().numpy(), ref), (n, n_per)
+        assert np.array_equal(u64(st).reshape(ref_st.shape), ref_st), (n, n_per)
+
+
+@pytest.mark.parametrize("knob", ["GZ_SEG_GUESS=1", "GZ_SEG_FALLBACK=1", "GZ_SEG=0"])
+def test_segmented_redecode_and_fallback_paths(knob):
+    """The rare paths of the segmented decode, forced: every speculative segment
+    re-decoded from its true entry (wrong guesses), every stream handed to the exact
+    warp loop, and the path disabled -- all give the default run's bits."""
+    import os
+    import subprocess
+    import sys
+
+    code = r"""
+import numpy as np, torch
+from paper_2405_19493_b200 import streams
+res = []
+for source, alg in (("splitmix", "ziggurat"), ("lcg48", "modified-ziggurat")):
+    st = streams.config_states("c1" if source == "splitmix" else "c4", 0, 500)
+    out = torch.empty((500, 3000), dtype=torch.float64, device="cuda")
+    streams.fill_gaussians_streams(alg, source, st, out)
+    v = out.cpu().numpy().view(np.uint64)
+    res.append((int(np.bitwise_xor.reduce(v.ravel())), v[:, -1].tobytes().hex()[:48], st.cpu().numpy().tobytes().hex()[:64]))
+print(repr(res))
+"""
+    outs = []
+    for env_kv in ("", knob):
+        env = dict(os.environ)
+        for k in ("GZ_SEG", "GZ_SEG_GUESS", "GZ_SEG_FALLBACK"):
+            env.pop(k, None)
+        if env_kv:
+            k, v = env_kv.split("=")
+            env[k] = v
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                           cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(r.stdout.strip().splitlines()[-1])
+    assert outs[0] == outs[1]
