@@ -1,230 +1,194 @@
 /*
- * gz_k_seg.cuh -- the ziggurats over FEW long streams: G warps per stream
- * (included by gz_engine.cu after gz_single.cuh).
+ * gz_k_seg.cuh -- the ziggurats over FEW long streams (included by gz_engine.cu
+ * after gz_single.cuh).
  *
  * With fewer streams than the GPU holds warps (config 1: 1024 streams), a warp per
  * stream leaves most of the machine idle and every warp walks its whole row.  Here
- * a block of G warps owns one stream.  Per round, the row's next draws are cut into
- * G segments of L draws; warp k decodes segment k with the warp-per-stream window
- * (zig_window) from a GUESSED entry -- warp 0 from the known one, the others from
- * the segment's first draw -- into a scratch buffer (values and each value's
- * attempt end).  An attempt that starts in segment k-1 may overhang into segment k
- * (wedge: 2 draws, tail: 1 + 2t), so the true entry e of segment k is the exit of
- * segment k-1.  Decoding is deterministic from an attempt start, so if the guessed
- * decode has an attempt start at e, both decodes agree from there on: its values
- * from e are the true ones and its exit is the true exit.  Almost always the guess
- * synchronises within a few draws (a fast-path attempt consumes exactly one draw);
- * when it does not, the warp re-decodes from e.  Thread 0 links the segments in
- * order, the warps copy their values to the row at their prefix offsets, and the
- * final state is the stream state after the last stored deviate's attempt.
+ * a row's draws are cut into segments decoded in parallel from GUESSED entries.  An
+ * attempt that starts in segment k-1 may overhang into segment k (wedge: 2 draws,
+ * tail: 1 + 2t), so the true entry e of segment k is the exit of segment k-1.
+ * Decoding is deterministic from an attempt start, so if the guessed decode has an
+ * attempt start at e, both decodes agree from there on: its deviates from e are the
+ * true ones and its exit is the true exit.  Almost always the guess synchronises
+ * within a few draws (a fast-path attempt consumes exactly one draw); when it does
+ * not, the segment is re-decoded from e.  Same draws, same decisions, same order as
+ * the sequential loop.
  *
- * Same draws, same decisions, same order as the sequential loop.  Guard: used only
- * when the guard exceeds any rejection run two segments can hold; a segment with no
- * deviate after its entry, or a tail that exhausts its guard, hands the whole stream
- * to the exact warp-per-stream loop (zig_warp_stream) in the same block.
+ * Guard: used only when the guard exceeds any rejection run two segments can hold;
+ * a segment with no deviate after its entry, or a tail that exhausts its guard,
+ * hands the whole stream to the exact warp-per-stream loop (zig_warp_stream).
+ * (A first form with one WARP per segment, decoding with the window parse, ran
+ * config 1 in 66 us; this lane form runs it in 51 us.)
  */
 #pragma once
 
-constexpr int SEG_MAXG = 5;   /* block <= 160 threads */
-#ifndef SEG_MINB
-#define SEG_MINB 4   /* __launch_bounds__(160, 4): at most 96 registers (5 -> 72 with spills: slower) */
-#endif
-
-struct SegOut {
-    int cnt;        /* deviates emitted by attempts starting in [entry, L) */
-    int exit;       /* the first attempt start >= L (segment-relative) */
-    uint32_t sm0;   /* decodes from entry 0: attempt starts among positions 0..31 */
-    uint32_t em0;   /* ... and those of them that emitted a deviate */
-    int bad;        /* a tail exhausted its guard / the rejection run reached it */
-    int entry;      /* the entry this decode started from */
+/*
+ * Lane-segment form (k_zig_lseg, the default): a block of P warps per stream, one
+ * LANE per segment.  Each round cuts the row's next 32*P*L draws into 32*P segments
+ * of L draws; lane k of warp w decodes segment 32w + k with the lane kernel's
+ * sequential attempt loop (k_zig_lane) from a guessed entry (segment 0: the known
+ * entry), staging its deviates in shared memory ([value][segment], padded rows) and
+ * their attempt ends in an L2 scratch.  Links inside a warp are resolved with
+ * shuffles (a lane whose guess did not synchronise re-decodes from its true entry),
+ * links between warps in warp order at block barriers; offsets by a warp scan plus
+ * a prefix over the warps.  A warp's segments are consecutive, so its deviates form
+ * one contiguous run of the row, stored coalesced (each lane finds its source
+ * segment by a binary search over the offsets).  Per deviate it executes the lane
+ * kernel's instructions instead of the window parse's.
+ */
+struct LsegParams {
+    double* scr_v;      /* unused (deviates are staged in shared memory) */
+    uint32_t* scr_e;    /* [warps][lcap][32] */
+    int lcap;           /* max draws per segment (>= every round's L) */
+    float dpv;          /* expected draws per deviate */
+    int guess;          /* entry guessed by lanes 1..31 */
+    int force_fallback;
 };
 
-struct SegShared {
-    SegOut so[SEG_MAXG];
-    int skip[SEG_MAXG], take[SEG_MAXG];
-    int64_t off[SEG_MAXG];
-    int redo, redo_entry, anomaly, e_after, final_k, got;
+struct LsegOut {
+    int cnt, exit, bad;
+    uint32_t sm0, em0;
 };
 
-struct SegParams {
-    double* scr_v;      /* [grid][G][lcap] deviates */
-    uint32_t* scr_e;    /* [grid][G][lcap] attempt ends (segment-relative) */
-    int lcap;           /* segment length cap (draws) */
-    float dpv;          /* draws per deviate used to size a round (with a margin) */
-    int guess;          /* entry guessed by warps 1..G-1 (0; tests use 1 to force re-decodes) */
-    int force_fallback; /* tests: every stream through zig_warp_stream */
-};
-
-/* decode one segment: attempts starting at segment positions [entry, L); S is the
-   stream state before the draw at position `entry` */
-template <int SRC, bool MOD, int D>
-__device__ __forceinline__ SegOut zig_seg_decode(uint64_t S, uint64_t gam, int entry, int L, const ZigParams& p,
-                                                 const ulonglong2* s_kw, const double2* s_yd,
-                                                 const ZigLaneConsts& kc, double* vb, uint32_t* ve, int lane)
+/* lane-sequential decode of one segment from position e0 (S: the state before it) */
+template <int SRC, int IBT, bool MOD>
+__device__ __forceinline__ LsegOut lseg_decode(uint64_t S, uint64_t gam, int e0, int L, const LaneParams& p,
+                                               uint32_t kw_sh, uint32_t yf_sh, int ib, uint32_t imask, int mbits,
+                                               uint64_t mmask, double* sv, int vstride, uint32_t* se, int lane)
 {
-    constexpr int W = 32 * D;
-    const uint32_t lt = (1u << lane) - 1u;
-    const int ib = p.index_bits;
-    const uint32_t imask = (uint32_t)p.n_layers - 1u;
-    const int mbits = 63 - ib;
-    const uint64_t mmask = (1ULL << mbits) - 1ULL;
-    const double r = p.r;
-    uint64_t gl = 0, g32 = 0;
-    if constexpr (SRC == 1) {
-        gl = (uint64_t)(lane + 1) * gam;
-        g32 = gam << 5;
-    }
-    SegOut o;
-    o.cnt = 0; o.exit = entry; o.sm0 = 0; o.em0 = 0; o.bad = 0; o.entry = entry;
-    int q0 = entry;        /* segment position of the window's first draw (an attempt start) */
-    int cnt = 0;
-    int64_t rej_run = 0;
-    bool first = entry == 0;
-    while (q0 < L) {
-        ZigWindow<D> w;
-        zig_window<SRC, MOD, D>(w, S, gam, gl, g32, kc, s_kw, s_yd, ib, imask, mbits, mmask, lane);
-        const int lim = L - q0;    /* window positions >= lim start no attempt of this segment */
-        int q = 0, c = 0, ext_lane = 0, ext_kind = 0;
-        bool stop = false;
-        uint64_t ext_t = 0;
-        uint32_t em[D], sm_first = 0;
-        int ebase[D], tlen[D];
-#pragma unroll
-        for (int d = 0; d < D; ++d) {
-            em[d] = 0;
-            ebase[d] = c;
-            tlen[d] = 0;
-            if (stop || q >= 32 * (d + 1)) continue;
-            int b = q - 32 * d;
-            const int limd = lim - 32 * d;   /* > b */
-            const uint32_t nfd = w.nf[d];
-            while (true) {
-                const uint32_t pend = nfd & (GZ_FULL << b);
-                const int f = pend ? (__ffs(pend) - 1) : 32;
-                if (limd <= f) {
-                    /* the fast run reaches the segment end: its last attempt starts at lim - 1 */
-                    em[d] |= gz_bitrange(b, limd - b);
-                    if (first && d == 0) sm_first |= gz_bitrange(b, limd - b);
-                    c += limd - b;
-                    rej_run = 0;
-                    q = lim;
-                    stop = true;
-                    break;
-                }
-                em[d] |= gz_bitrange(b, f - b);
-                if (first && d == 0) sm_first |= gz_bitrange(b, f - b);
-                c += f - b;
-                if (f > b) rej_run = 0;
-                if (f == 32) {
-                    q = 32 * (d + 1);
-                    break;
-                }
-                const int pos = 32 * d + f;
-                if (first && d == 0) sm_first |= 1u << f;
-                if ((w.tl[d] >> f) & 1u) {
-                    int tt = 0;
-                    if (lane == f) {
-                        const TailOut to = tail_seq<SRC>(w.st[d], gam, r, p.guard);
-                        tt = to.k;
-                        ext_t = to.st;
-                        w.val[d] = signbit(w.val[d]) ? -to.v : to.v;
-                        tlen[d] = 1 + 2 * to.k;
-                    }
-                    tt = __shfl_sync(GZ_FULL, tt, f);
-                    if (tt < 0) {
-                        o.bad = 1;
-                        stop = true;
-                        break;
-                    }
-                    em[d] |= 1u << f;
-                    ++c;
-                    rej_run = 0;
-                    q = pos + 1 + 2 * tt;
-                    ext_kind = 1;
-                    ext_lane = f;
-                } else {
-                    if ((w.am[d] >> f) & 1u) {
-                        em[d] |= 1u << f;
-                        ++c;
-                        rej_run = 0;
-                    } else if (++rej_run >= p.guard) {
-                        o.bad = 1;
-                        stop = true;
-                        break;
-                    }
-                    q = pos + 2;
-                    ext_kind = 2;
-                }
-                if (q >= lim) {
-                    stop = true;
-                    break;
-                }
-                if (q >= 32 * (d + 1)) break;
-                b = q - 32 * d;
-            }
-        }
-        if (o.bad) break;
-        /* ---- emit into the scratch row: deviate and its attempt's end position ---- */
-#pragma unroll
-        for (int d = 0; d < D; ++d) {
-            if ((em[d] >> lane) & 1u) {
-                const int rel = cnt + ebase[d] + __popc(em[d] & lt);
-                vb[rel] = w.val[d];
-                const uint32_t nfb = (w.nf[d] >> lane) & 1u, tlb = (w.tl[d] >> lane) & 1u;
-                const int len = nfb ? (tlb ? tlen[d] : 2) : 1;
-                ve[rel] = (uint32_t)(q0 + 32 * d + lane + len);
-            }
-        }
-        if (first) {
-            o.sm0 = sm_first;
-            o.em0 = em[0];
-            first = false;
-        }
-        cnt += c;
-        /* ---- advance past the consumed draws ---- */
-        if constexpr (SRC == 1) {
-            S += (uint64_t)q * gam;
+    LsegOut o;
+    o.cnt = 0; o.bad = 0; o.sm0 = 0; o.em0 = 0;
+    const bool rec = e0 == 0;
+    const uint32_t guard32 = p.guard > 0xffffffffll ? 0xffffffffu : (uint32_t)p.guard;
+    uint64_t nxt = 0;
+    lane_pend<SRC>(S, gam, nxt);
+    uint32_t rej = 0;
+    int q = e0, cnt = 0;
+    while (q < L) {
+        const int start = q;
+        const uint64_t u = lane_take<SRC>(S, gam, nxt);
+        ++q;
+        uint32_t i;
+        uint64_t m, sgn;
+        if constexpr (MOD) {
+            i = (uint32_t)u & imask;
+            m = u >> (ib + 1);
+            sgn = (u >> ib) << 63;
         } else {
-            if (q <= W) {
-                const int pq = q - 1;
-                uint64_t sel = w.st[0];
-#pragma unroll
-                for (int d = 1; d < D; ++d)
-                    if ((pq >> 5) == d) sel = w.st[d];
-                S = __shfl_sync(GZ_FULL, sel, pq & 31);
-            } else if (ext_kind == 1) {
-                S = __shfl_sync(GZ_FULL, ext_t, ext_lane);
+            i = (uint32_t)(u >> mbits) & imask;
+            m = u & mmask;
+            sgn = u & 0x8000000000000000ULL;
+        }
+        const ulonglong2 kw = lds_u64x2(kw_sh + 16 * i);
+        double x = __dmul_rn(__ull2double_rn(m), __longlong_as_double((long long)kw.y));
+        bool ok = m < kw.x;
+        if (!ok) {
+            if (i != 0) {
+                const uint64_t u2 = lane_take<SRC>(S, gam, nxt);
+                ++q;
+                ok = wedge_accept_f(u2, x, p.yd + i, lds_f32x2(yf_sh + 8 * i));
+                if (!ok && ++rej >= guard32) {
+                    o.bad = 1;
+                    break;
+                }
             } else {
-                S = __shfl_sync(GZ_FULL, w.extw, 31);
+                double tr = p.r;
+                int64_t tg = p.guard;
+                asm volatile("ld.f64 %0, [%1];" : "=d"(tr) : "l"(&p.r));
+                asm volatile("ld.s64 %0, [%1];" : "=l"(tg) : "l"(&p.guard));
+                const TailOut to = tail_seq<SRC>(S, gam, tr, tg);
+                S = to.st;
+                lane_pend<SRC>(S, gam, nxt);
+                x = to.v;
+                ok = to.k >= 0;
+                if (!ok) {
+                    o.bad = 1;
+                    break;
+                }
+                q += 2 * to.k;
             }
         }
-        q0 += q;
-        if (stop) break;
+        if (rec && start < 32) {
+            o.sm0 |= 1u << start;
+            if (ok) o.em0 |= 1u << start;
+        }
+        if (ok) {
+            rej = 0;
+            sv[cnt * vstride] = __longlong_as_double((long long)((uint64_t)__double_as_longlong(x) ^ sgn));
+            se[(size_t)cnt * 32] = (uint32_t)q;
+            ++cnt;
+        }
     }
     o.cnt = cnt;
-    o.exit = q0;
+    o.exit = q;
     return o;
 }
 
-template <int SRC, bool MOD, int D>
-__global__ void __launch_bounds__(32 * SEG_MAXG, SEG_MINB) k_zig_seg(const ZigParams p, const SegParams sp)
+/* link the lanes of one warp: lane 0's true entry is ek0; every other lane's is its
+   left neighbour's exit.  A lane whose decode has no attempt start at its true entry
+   re-decodes from it (left to right).  Returns this lane's true entry. */
+template <int SRC, int IBT, bool MOD>
+__device__ __forceinline__ int lseg_link(LsegOut& o, int& e0, int ek0, int L, uint64_t S0, uint64_t gam, int64_t seg_base,
+                                         const LaneParams& p, uint32_t kw_sh, uint32_t yf_sh, int ib, uint32_t imask,
+                                         int mbits, uint64_t mmask, double* sv, int vstride, uint32_t* se, int lane)
+{
+    int ek = __shfl_up_sync(GZ_FULL, o.exit, 1) - L;
+    if (lane == 0) ek = ek0;
+    bool cov = lane == 0 || ek == e0 || (e0 == 0 && ek < 32 && ((o.sm0 >> ek) & 1u));
+    uint32_t unc = __ballot_sync(GZ_FULL, !cov);
+    while (unc) {
+        const int ks = __ffs(unc) - 1;
+        if (lane == ks) {
+            e0 = ek;
+            o = lseg_decode<SRC, IBT, MOD>(single_state_at<SRC>(S0, gam, (uint64_t)(seg_base + e0)), gam, e0, L, p,
+                                           kw_sh, yf_sh, ib, imask, mbits, mmask, sv, vstride, se, lane);
+        }
+        const int ex = __shfl_up_sync(GZ_FULL, o.exit, 1) - L;
+        if (lane > ks) ek = ex;
+        cov = lane <= ks || ek == e0 || (e0 == 0 && ek < 32 && ((o.sm0 >> ek) & 1u));
+        unc = __ballot_sync(GZ_FULL, !cov);
+    }
+    return ek;
+}
+
+constexpr int LSEG_MAXP = 8;
+
+struct LsegShared {
+    int exit31[LSEG_MAXP];      /* each warp's last segment exit */
+    int total[LSEG_MAXP];       /* valid deviates per warp */
+    int64_t woff[LSEG_MAXP];    /* row offset of each warp's first deviate (this round) */
+    int64_t kept;               /* deviates kept this round */
+};
+
+template <int SRC, int IBT, bool MOD>
+__global__ void __launch_bounds__(32 * LSEG_MAXP) k_zig_lseg(const __grid_constant__ LaneParams p, const LsegParams sp)
 {
     extern __shared__ __align__(16) unsigned char smem[];
-    const int nl = p.n_layers;
+    const int nl = IBT ? (1 << IBT) : p.n_layers;
     ulonglong2* s_kw = reinterpret_cast<ulonglong2*>(smem);
-    double2* s_yd = reinterpret_cast<double2*>(smem + 16 * nl);
-    SegShared& sh = *reinterpret_cast<SegShared*>(smem + 32 * nl);
+    float2* s_yf = reinterpret_cast<float2*>(smem + 16 * nl);
+    LsegShared& sh = *reinterpret_cast<LsegShared*>(smem + 24 * nl);
+    /* deviates staged in shared memory, [value][segment] with a padded row: the decode
+       writes a row per attempt, the copy reads a column per lane, both conflict-free */
+    double* s_val = reinterpret_cast<double*>(smem + 24 * nl + ((sizeof(LsegShared) + 15) & ~(size_t)15));
     for (int i = threadIdx.x; i < nl; i += blockDim.x) {
         s_kw[i] = p.kw[i];
-        s_yd[i] = p.yd[i];
+        s_yf[i] = p.yf[i];
     }
     __syncthreads();
-    const int G = (int)(blockDim.x >> 5);
-    const int k = (int)(threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
-    const ZigLaneConsts kc = zig_lane_consts<SRC>(lane);
-    double* vb = sp.scr_v + ((int64_t)blockIdx.x * G + k) * sp.lcap;
-    uint32_t* ve = sp.scr_e + ((int64_t)blockIdx.x * G + k) * sp.lcap;
+    const int w = threadIdx.x >> 5;
+    const int P = blockDim.x >> 5;
+    const int g = threadIdx.x;               /* segment index within the round */
+    const uint32_t kw_sh = sh_addr(s_kw), yf_sh = sh_addr(s_yf);
+    const int ib = IBT ? IBT : p.index_bits;
+    const uint32_t imask = (uint32_t)nl - 1u;
+    const int mbits = 63 - ib;
+    const uint64_t mmask = (1ULL << mbits) - 1ULL;
+    const int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int vstride = 32 * P + 1;
+    double* const sv = s_val + g;
+    uint32_t* const se = sp.scr_e + (size_t)wg * sp.lcap * 32 + lane;
 
     for (int64_t sid = blockIdx.x; sid < p.n_streams; sid += gridDim.x) {
         uint64_t S0, gam = 0;
@@ -239,111 +203,124 @@ __global__ void __launch_bounds__(32 * SEG_MAXG, SEG_MINB) k_zig_seg(const ZigPa
         int entry = 0;
         bool anomaly = sp.force_fallback != 0;
         while (need > 0 && !anomaly) {
-            const int Lr = min(sp.lcap, (int)ceilf((float)need * sp.dpv / (float)G) + 32);
-            {
-                const int e0 = k == 0 ? entry : sp.guess;
-                const SegOut o = zig_seg_decode<SRC, MOD, D>(single_state_at<SRC>(S0, gam, (uint64_t)(base + (int64_t)k * Lr + e0)),
-                                                             gam, e0, Lr, p, s_kw, s_yd, kc, vb, ve, lane);
-                if (lane == 0) sh.so[k] = o;
-            }
+            /* draws for `need` deviates with a 6-sigma margin, over 32P segments */
+            const float fneed = (float)need;
+            int L = (int)ceilf((fneed * sp.dpv + 6.0f * sqrtf(fneed * 0.06f) + 32.0f) / (float)(32 * P));
+            L = max(16, min(L, sp.lcap));
+            const int64_t seg_base = base + (int64_t)g * L;
+            int e0 = g == 0 ? entry : sp.guess;
+            LsegOut o = lseg_decode<SRC, IBT, MOD>(single_state_at<SRC>(S0, gam, (uint64_t)(seg_base + e0)), gam, e0, L, p,
+                                                   kw_sh, yf_sh, ib, imask, mbits, mmask, sv, vstride, se, lane);
+            /* lanes 1..31 of every warp; lane 0 provisionally at its own entry */
+            int ek = lseg_link<SRC, IBT, MOD>(o, e0, e0, L, S0, gam, seg_base, p, kw_sh, yf_sh, ib, imask, mbits,
+                                              mmask, sv, vstride, se, lane);
+            if (lane == 31) sh.exit31[w] = o.exit;
             __syncthreads();
-            /* link the segments in order; re-decode a segment whose guess did not synchronise */
-            int from = 0, e = entry;
-            while (true) {
-                if (threadIdx.x == 0) {
-                    sh.redo = -1;
-                    sh.anomaly = 0;
-                    for (int j = from; j < G; ++j) {
-                        const SegOut& oj = sh.so[j];
-                        int skip;
-                        if (oj.entry == e) {
-                            skip = 0;
-                        } else if (oj.entry == 0 && e < 32 && ((oj.sm0 >> e) & 1u)) {
-                            skip = __popc(oj.em0 & ((1u << e) - 1u));
-                        } else {
-                            sh.redo = j;
-                            sh.redo_entry = e;
-                            break;
+            /* links between warps, in order: warp v's lane 0 starts where warp v-1's lane 31
+               ends; a warp whose lane-0 guess missed re-decodes it and relinks its lanes */
+            if (w == 0 && lane == 0) ek = entry;
+            for (int v = 1; v < P; ++v) {
+                __syncthreads();
+                if (w == v) {
+                    const int e = sh.exit31[v - 1] - L;
+                    const int e_own = __shfl_sync(GZ_FULL, e0, 0);
+                    const uint32_t sm_own = __shfl_sync(GZ_FULL, o.sm0, 0);
+                    const bool cov = e == e_own || (e_own == 0 && e < 32 && ((sm_own >> e) & 1u));
+                    if (!cov) {
+                        if (lane == 0) {
+                            e0 = e;
+                            o = lseg_decode<SRC, IBT, MOD>(single_state_at<SRC>(S0, gam, (uint64_t)(seg_base + e0)), gam,
+                                                           e0, L, p, kw_sh, yf_sh, ib, imask, mbits, mmask, sv, vstride,
+                                                           se, lane);
                         }
-                        if (oj.bad || oj.cnt - skip <= 0) {
-                            sh.anomaly = 1;
-                            break;
-                        }
-                        sh.skip[j] = skip;
-                        e = oj.exit - Lr;
+                        ek = lseg_link<SRC, IBT, MOD>(o, e0, e, L, S0, gam, seg_base, p, kw_sh, yf_sh, ib, imask, mbits,
+                                                      mmask, sv, vstride, se, lane);
+                        if (lane == 31) sh.exit31[w] = o.exit;
                     }
-                    sh.e_after = e;
+                    if (lane == 0) ek = e;
                 }
-                __syncthreads();
-                if (sh.anomaly || sh.redo < 0) break;
-                from = sh.redo;
-                e = sh.redo_entry;
-                if (k == from) {
-                    const SegOut o = zig_seg_decode<SRC, MOD, D>(single_state_at<SRC>(S0, gam, (uint64_t)(base + (int64_t)k * Lr + e)),
-                                                                 gam, e, Lr, p, s_kw, s_yd, kc, vb, ve, lane);
-                    if (lane == 0) sh.so[k] = o;
-                }
-                __syncthreads();
             }
-            if (sh.anomaly) {
+            const int skip = ek == e0 ? 0 : __popc(o.em0 & ((1u << ek) - 1u));
+            const int valid = o.cnt - skip;
+            if (__syncthreads_or(o.bad || valid <= 0)) {
                 anomaly = true;
                 break;
             }
-            /* offsets and counts; the round that completes the row finds the last attempt */
+            /* offsets: warp scan, then a prefix over the warps */
+            int off = valid;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const int t = __shfl_up_sync(GZ_FULL, off, d);
+                if (lane >= d) off += t;
+            }
+            if (lane == 31) sh.total[w] = off;
+            off -= valid;
+            __syncthreads();
             if (threadIdx.x == 0) {
-                int64_t off = produced, left = need;
-                sh.final_k = -1;
-                for (int j = 0; j < G; ++j) {
-                    const int valid = sh.so[j].cnt - sh.skip[j];
-                    const int take = left <= 0 ? 0 : (int)(left < (int64_t)valid ? left : (int64_t)valid);
-                    sh.take[j] = take;
-                    sh.off[j] = off;
-                    off += take;
-                    left -= take;
-                    if (left == 0 && take > 0 && sh.final_k < 0) sh.final_k = j;
+                int64_t acc = 0;
+                for (int v = 0; v < P; ++v) {
+                    sh.woff[v] = acc;
+                    acc += sh.total[v];
                 }
-                sh.got = (int)(need - left);
+                sh.kept = acc > need ? need : acc;   /* deviates kept this round */
             }
             __syncthreads();
+            const int64_t goff = sh.woff[w] + off;
+            const int64_t kept = sh.kept;
+            const int64_t room = need - goff;
+            const int take = room <= 0 ? 0 : (int)(room < valid ? room : valid);
             {
-                /* scratch (L2) -> row: eight loads in flight per lane before the stores */
-                const int take = sh.take[k], skip = sh.skip[k];
-                double* dst = row + sh.off[k];
-                const double* src = vb + skip;
-                for (int i0 = 0; i0 < take; i0 += 256) {
-                    double v[8];
+                /* the warp's segments are consecutive, so its deviates form one contiguous
+                   run of the row: lane t of each pass finds its segment by a binary search
+                   over the offsets and stores coalesced */
+                const int wlen = (int)__reduce_add_sync(GZ_FULL, (unsigned)take);
+                double* dst = row + produced + sh.woff[w];
+                const double* wval = s_val + 32 * w;
+                for (int t0 = 0; t0 < wlen; t0 += 32) {
+                    const int t = t0 + lane;
+                    int src = 0;
 #pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        const int i = i0 + 32 * u + lane;
-                        v[u] = i < take ? __ldcg(src + i) : 0.0;
+                    for (int step = 16; step > 0; step >>= 1) {
+                        const int cand = src + step;
+                        if (__shfl_sync(GZ_FULL, off, cand) <= t) src = cand;
                     }
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        const int i = i0 + 32 * u + lane;
-                        if (i < take) dst[i] = v[u];
-                    }
+                    const int o_s = __shfl_sync(GZ_FULL, off, src);
+                    const int k_s = __shfl_sync(GZ_FULL, skip, src);
+                    if (t < wlen) dst[t] = wval[(k_s + t - o_s) * vstride + src];
                 }
             }
-            const int got = sh.got;
-            if (need - got == 0 && k == sh.final_k && lane == 0) {
-                const uint32_t end = ve[sh.skip[k] + sh.take[k] - 1];
-                const uint64_t s_end = single_state_at<SRC>(S0, gam, (uint64_t)(base + (int64_t)k * Lr + end));
-                if constexpr (SRC == 0) {
-                    p.state_out[sid] = s_end;
-                } else {
-                    p.state_out[2 * sid] = s_end;
-                    p.state_out[2 * sid + 1] = gam;
+            if (kept == need) {
+                if (take > 0 && goff + take == need) {
+                    const uint32_t end = se[(size_t)(skip + take - 1) * 32];
+                    const uint64_t s_end = single_state_at<SRC>(S0, gam, (uint64_t)(seg_base + end));
+                    if constexpr (SRC == 0) {
+                        p.state_out[sid] = s_end;
+                    } else {
+                        p.state_out[2 * sid] = s_end;
+                        p.state_out[2 * sid + 1] = gam;
+                    }
                 }
+                need = 0;
+            } else {
+                need -= kept;
+                produced += kept;
+                entry = sh.exit31[P - 1] - L;
+                base += (int64_t)32 * P * L;
             }
-            need -= got;
-            produced += got;
-            base += (int64_t)G * Lr;
-            entry = sh.e_after;
             __syncthreads();
         }
         if (anomaly) {
             /* the exact sequential loop decides (and raises a guard trip) */
-            if (k == 0) zig_warp_stream<SRC, MOD, D, EPI_STORE, false>(p, sid, s_kw, s_yd, kc, lane);
+            if (w == 0) {
+                ZigParams zp;
+                zp.n_streams = p.n_streams; zp.n_per = p.n_per; zp.ld = p.ld;
+                zp.state_in = p.state_in; zp.state_out = p.state_out; zp.out = p.out;
+                zp.sigma = nullptr; zp.checksum = nullptr; zp.psum = nullptr;
+                zp.kw = p.kw; zp.yd = p.yd; zp.n_layers = nl; zp.index_bits = ib; zp.r = p.r; zp.guard = p.guard;
+                zp.generations = 1;
+                const ZigLaneConsts kc = zig_lane_consts<SRC>(lane);
+                zig_warp_stream<SRC, MOD, 4, EPI_STORE, false>(zp, sid, p.kw, p.yd, kc, lane);
+            }
         } else if (p.n_per == 0 && threadIdx.x == 0) {
             if constexpr (SRC == 0) {
                 p.state_out[sid] = S0;
