@@ -161,7 +161,7 @@ struct LsegShared {
 };
 
 template <int SRC, int IBT, bool MOD>
-__global__ void __launch_bounds__(32 * LSEG_MAXP) k_zig_lseg(const __grid_constant__ LaneParams p, const LsegParams sp)
+__global__ void __launch_bounds__(32 * LSEG_MAXP, SRC == 1 ? 3 : 2) k_zig_lseg(const __grid_constant__ LaneParams p, const LsegParams sp)
 {
     extern __shared__ __align__(16) unsigned char smem[];
     const int nl = IBT ? (1 << IBT) : p.n_layers;
