@@ -66,43 +66,56 @@ __device__ __forceinline__ uint64_t single_state_at(uint64_t s0, uint64_t gam, u
 
 /* ------------------------------------------------------------------ polar */
 
-/* per-block state base (thread 0) and per-thread offset (4t LCG steps / 2t draws) */
+/* SP_K consecutive attempts per thread: the per-thread jump and the block's base jump
+   are paid once per SP_K attempts */
+constexpr int SP_K = 8;
+constexpr int SP_BLOCK = SP_T * SP_K;   /* attempts per block */
+
+/* the state before attempt jb + SP_K*t of the block (thread 0 jumps to the block
+   base, every thread jumps 4*SP_K*t LCG steps / 2*SP_K*t draws from it) */
 template <int SRC>
-__device__ __forceinline__ uint64_t polar_single_state(const uint64_t* st0, uint64_t& gam, int64_t j0, uint64_t* s_base)
+__device__ __forceinline__ uint64_t polar_single_state(const uint64_t* st0, uint64_t& gam, int64_t jb, uint64_t* s_base)
 {
     const int t = threadIdx.x;
-    uint64_t s0;
+    const uint64_t s0 = st0[0];
     if constexpr (SRC == 0) {
-        s0 = st0[0];
         gam = 0;
-    } else {
-        s0 = st0[0];
-        gam = st0[1];
-    }
-    if constexpr (SRC == 0) {
-        if (t == 0) *s_base = single_state_at<0>(s0, 0, 2 * (uint64_t)j0);
+        if (t == 0) *s_base = single_state_at<0>(s0, 0, 2 * (uint64_t)jb);
         __syncthreads();
         uint64_t A, C;
-        lcg_jump_n(4 * (uint64_t)t, A, C);
+        lcg_jump_n(4 * (uint64_t)SP_K * t, A, C);
         return (A * *s_base + C) & GZ_MASK48;
     } else {
-        return s0 + (uint64_t)(2 * (j0 + t)) * gam;
+        gam = st0[1];
+        return s0 + (uint64_t)(2 * (jb + (int64_t)SP_K * t)) * gam;
     }
 }
 
-/* one polar attempt from state S (the state before its first draw): v1, v2, s and
-   the state after its two draws */
+/* one polar attempt from state S (the state before its first draw): v1, v2, s; S
+   advances past its two draws */
 template <int SRC>
-__device__ __forceinline__ bool polar_single_attempt(uint64_t S, uint64_t gam, double& v1, double& v2, double& s,
-                                                     uint64_t& S_after)
+__device__ __forceinline__ bool polar_single_attempt(uint64_t& S, uint64_t gam, double& v1, double& v2, double& s)
 {
     const uint64_t ua = gz_next_seq<SRC>(S, gam);
     const uint64_t ub = gz_next_seq<SRC>(S, gam);
-    S_after = S;
     v1 = gz_unit53_pm1(ua);
     v2 = gz_unit53_pm1(ub);
     s = __dadd_rn(__dmul_rn(v1, v1), __dmul_rn(v2, v2));
     return s > 0.0 && s < 1.0;
+}
+
+/* this thread's SP_K attempts: bit k of the result = attempt k accepted */
+template <int SRC>
+__device__ __forceinline__ uint32_t polar_single_mask(uint64_t S, uint64_t gam, int64_t first, int64_t end)
+{
+    uint32_t m = 0;
+#pragma unroll
+    for (int k = 0; k < SP_K; ++k) {
+        double v1, v2, s;
+        const bool acc = polar_single_attempt<SRC>(S, gam, v1, v2, s);
+        if (acc && first + k < end) m |= 1u << k;
+    }
+    return m;
 }
 
 /* pass 1: accepted attempts per block for attempts [j0, j0 + n_att) */
@@ -111,13 +124,12 @@ __global__ void __launch_bounds__(SP_T) k_polar_single_count(const uint64_t* st0
 {
     __shared__ uint64_t s_base;
     __shared__ int s_c[SP_T / 32];
-    const int64_t jb = j0 + (int64_t)blockIdx.x * SP_T;
+    const int64_t jb = j0 + (int64_t)blockIdx.x * SP_BLOCK;
     uint64_t gam;
     const uint64_t S = polar_single_state<SRC>(st0, gam, jb, &s_base);
-    double v1, v2, s;
-    uint64_t Sa;
-    const bool acc = (jb + threadIdx.x < j0 + n_att) && polar_single_attempt<SRC>(S, gam, v1, v2, s, Sa);
-    const int wc = __popc(__ballot_sync(GZ_FULL, acc));
+    const int64_t first = jb + (int64_t)SP_K * threadIdx.x;
+    const int c = __popc(polar_single_mask<SRC>(S, gam, first, j0 + n_att));
+    const int wc = __reduce_add_sync(GZ_FULL, (unsigned)c);
     if ((threadIdx.x & 31) == 0) s_c[threadIdx.x >> 5] = wc;
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -136,7 +148,25 @@ struct PolarSingleOut {
     uint64_t* state_out;
 };
 
-/* pass 2: transform and store the accepted pairs at their prefix rank */
+/* store pair k of the call (the odd call's last pair: one deviate + the spare) */
+__device__ __forceinline__ void polar_single_store(const PolarSingleOut& o, int64_t k, double v1, double v2, double mul)
+{
+    const double o1 = __dmul_rn(v1, mul), o2 = __dmul_rn(v2, mul);
+    if (o.odd && k == o.np - 1) {
+        o.out[2 * k] = o1;
+        if (o.spare_out) o.spare_out[0] = o2;
+    } else {
+        pair_store(o.out + 2 * k, o1, o2);
+    }
+}
+
+/*
+ * pass 2: every thread regenerates its SP_K attempts and writes its accepted pairs,
+ * in attempt order, to a block queue in shared memory; the block then transforms
+ * the queue with all threads -- glibc log's main branch at once, the near-1 pairs
+ * (s >= 1 - 2^-4) compacted into a list and transformed after -- and stores pair q
+ * of the queue at its prefix rank (coalesced).
+ */
 template <int SRC>
 __global__ void __launch_bounds__(SP_T) k_polar_single_emit(const uint64_t* st0, int64_t j0, int64_t n_att,
                                                             const int* prefix, PolarSingleOut o)
@@ -144,42 +174,84 @@ __global__ void __launch_bounds__(SP_T) k_polar_single_emit(const uint64_t* st0,
     __shared__ uint64_t s_base;
     __shared__ int s_c[SP_T / 32];
     __shared__ uint64_t s_log[256];
+    __shared__ double2 s_q[SP_BLOCK];
+    __shared__ short s_near[SP_BLOCK];
+    __shared__ int s_nn;
     const int64_t pre = prefix[blockIdx.x];
     const int64_t need = o.np - o.pairs_done;
     if (pre >= need) return;   /* block-uniform */
     for (int i = threadIdx.x; i < 256; i += SP_T) s_log[i] = g_log_tab[i];
-    const int64_t jb = j0 + (int64_t)blockIdx.x * SP_T;
+    if (threadIdx.x == 0) s_nn = 0;
+    const int64_t jb = j0 + (int64_t)blockIdx.x * SP_BLOCK;
     uint64_t gam;
-    const uint64_t S = polar_single_state<SRC>(st0, gam, jb, &s_base);
-    double v1, v2, s;
-    uint64_t Sa;
-    const bool acc = (jb + threadIdx.x < j0 + n_att) && polar_single_attempt<SRC>(S, gam, v1, v2, s, Sa);
-    const uint32_t bal = __ballot_sync(GZ_FULL, acc);
+    const uint64_t S0 = polar_single_state<SRC>(st0, gam, jb, &s_base);
+    const int64_t first = jb + (int64_t)SP_K * threadIdx.x, end = j0 + n_att;
+    const uint32_t m = polar_single_mask<SRC>(S0, gam, first, end);
+    /* block exclusive scan of the per-thread counts */
+    const int c = __popc(m);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    if (lane == 0) s_c[wid] = __popc(bal);
+    int incl = c;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const int t = __shfl_up_sync(GZ_FULL, incl, d);
+        if (lane >= d) incl += t;
+    }
+    if (lane == 31) s_c[wid] = incl;
     __syncthreads();
     int wbase = 0;
     for (int w = 0; w < wid; ++w) wbase += s_c[w];
-    const int64_t rank = pre + wbase + __popc(bal & ((1u << lane) - 1u));
-    if (acc && rank < need) {
-        const int64_t k = o.pairs_done + rank;   /* the call's pair index */
-        const double mul = polar_mul(s, s_log);
-        const double o1 = __dmul_rn(v1, mul), o2 = __dmul_rn(v2, mul);
-        if (o.odd && k == o.np - 1) {
-            o.out[2 * k] = o1;
-            if (o.spare_out) o.spare_out[0] = o2;
-        } else {
-            pair_store(o.out + 2 * k, o1, o2);
-        }
-        if (rank == need - 1) {
-            /* the call's last attempt: the stream continues after its two draws */
-            if constexpr (SRC == 0) {
-                o.state_out[0] = Sa & GZ_MASK48;
-            } else {
-                o.state_out[0] = Sa;
-                o.state_out[1] = gam;
+    int nq = 0;
+    for (int w = 0; w < SP_T / 32; ++w) nq += s_c[w];
+    int q = wbase + incl - c;
+    /* regenerate and queue the accepted pairs; the attempt of the call's last pair
+       leaves the stream state */
+    {
+        uint64_t S = S0;
+#pragma unroll
+        for (int k = 0; k < SP_K; ++k) {
+            double v1, v2, s;
+            polar_single_attempt<SRC>(S, gam, v1, v2, s);
+            if ((m >> k) & 1u) {
+                s_q[q] = make_double2(v1, v2);
+                if (pre + q == need - 1) {
+                    if constexpr (SRC == 0) {
+                        o.state_out[0] = S & GZ_MASK48;
+                    } else {
+                        o.state_out[0] = S;
+                        o.state_out[1] = gam;
+                    }
+                }
+                ++q;
             }
         }
+    }
+    __syncthreads();
+    const int nkeep = (int)(need - pre < nq ? need - pre : nq);
+    /* main branch: all threads; near-1 pairs are listed for the second pass */
+    for (int i = threadIdx.x; i < nkeep; i += SP_T) {
+        const double2 v = s_q[i];
+        const double s = __dadd_rn(__dmul_rn(v.x, v.x), __dmul_rn(v.y, v.y));
+        const bool near = (uint64_t)__double_as_longlong(s) >= 0x3fee000000000000ULL;
+        if (!near) {
+            const double mul = sqrt_rn_nb(div_rn_nb(__dmul_rn(-2.0, gz_log_core((uint64_t)__double_as_longlong(s), s_log)), s));
+            polar_single_store(o, o.pairs_done + pre + i, v.x, v.y, mul);
+        }
+        const uint32_t nb = __ballot_sync(__activemask(), near);
+        if (near) {
+            const int leader = __ffs(nb) - 1;
+            int base = 0;
+            if (lane == leader) base = atomicAdd(&s_nn, __popc(nb));
+            base = __shfl_sync(nb, base, leader);
+            s_near[base + __popc(nb & ((1u << lane) - 1u))] = (short)i;
+        }
+    }
+    __syncthreads();
+    const int nn = s_nn;
+    for (int t = threadIdx.x; t < nn; t += SP_T) {
+        const int i = s_near[t];
+        const double2 v = s_q[i];
+        const double s = __dadd_rn(__dmul_rn(v.x, v.x), __dmul_rn(v.y, v.y));
+        polar_single_store(o, o.pairs_done + pre + i, v.x, v.y, polar_mul(s, s_log));
     }
 }
 
