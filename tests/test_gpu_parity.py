@@ -803,3 +803,59 @@ print(repr(res))
         assert r.returncode == 0, r.stderr[-2000:]
         outs.append(r.stdout.strip().splitlines()[-1])
     assert outs[0] == outs[1]
+
+
+# ---- maximum sizes: one launch of more than 2^32 output elements ---------------
+
+@pytest.mark.parametrize("alg,source", [("polar", "lcg48"), ("ziggurat", "lcg48"),
+                                        ("modified-ziggurat", "splitmix")])
+def test_output_beyond_2p32_elements(alg, source):
+    """2^24 + 5 streams x 257 deviates (4.3e9 elements, 34.5 GB) in one call: the rows
+    whose element offsets straddle 2^31 and 2^32, and the first and last rows, equal
+    the oracle bit for bit (states and polar spares included); the whole output equals
+    a second kernel's (polar: the fused-witness kernel; ziggurats: the warp-per-stream
+    kernel) bit for bit."""
+    n, n_per = (1 << 24) + 5, 257
+    need = 2 * n * n_per * 8 + (1 << 30)
+    if torch.cuda.mem_get_info()[0] < need:
+        pytest.skip("needs ~70 GB of free device memory")
+    rng = np.random.default_rng(2032)
+    st_np = rng.integers(0, 2 ** 63, size=(n, 1 if source == "lcg48" else 2), dtype=np.uint64)
+    if source == "lcg48":
+        st_np = (st_np[:, 0] & np.uint64((1 << 48) - 1)).copy()
+    else:
+        st_np[:, 1] |= np.uint64(1)              # odd gammas
+    rows = sorted({0, 1, 2, n - 2, n - 1,
+                   (1 << 31) // n_per - 1, (1 << 31) // n_per, (1 << 31) // n_per + 1,
+                   (1 << 32) // n_per - 1, (1 << 32) // n_per, (1 << 32) // n_per + 1})
+    kw = {}
+    if alg == "polar":
+        kw = dict(spare=torch.zeros(n, dtype=torch.float64, device=DEV),
+                  has_spare=torch.zeros(n, dtype=torch.uint8, device=DEV))
+    st = dev_states(source, st_np)
+    out = torch.empty((n, n_per), dtype=torch.float64, device=DEV)
+    streams.fill_gaussians_streams(alg, source, st, out, **kw)
+    ref, ref_st, ref_sp, ref_has, status = O.fill_gaussians(alg, source, st_np[rows], n_per)
+    assert status == 0
+    idx = torch.tensor(rows, device=DEV)
+    assert bits_equal(out[idx].cpu().numpy(), ref)
+    assert np.array_equal(u64(st).reshape(n, -1)[rows], ref_st.reshape(len(rows), -1))
+    if alg == "polar":
+        assert np.array_equal(kw["has_spare"][idx].cpu().numpy(), ref_has)
+        assert bits_equal(kw["spare"][idx].cpu().numpy(), ref_sp)
+    # the same launch through a second kernel, compared over all 4.3e9 elements
+    out2 = torch.empty_like(out)
+    st2 = dev_states(source, st_np)
+    if alg == "polar":
+        ck = torch.zeros(n, dtype=torch.int64, device=DEV)
+        streams.fill_gaussians_streams(alg, source, st2, out2, checksum=ck,
+                                       spare=torch.zeros(n, dtype=torch.float64, device=DEV),
+                                       has_spare=torch.zeros(n, dtype=torch.uint8, device=DEV))
+    else:
+        streams.set_kernel_policy("warp")
+        try:
+            streams.fill_gaussians_streams(alg, source, st2, out2)
+        finally:
+            streams.set_kernel_policy("auto")
+    assert torch.equal(out.view(torch.int64), out2.view(torch.int64))
+    assert torch.equal(st, st2)
