@@ -229,8 +229,20 @@ def compute_bounds(variates_per_s, hbm_gbs, clocks):
     b = {"hbm": hbm_gbs * 1e9 / 8, "int": sms * hz * INT_OPS_PER_SM_CLK / INT_OPS_PER_VARIATE,
          "fp64": sms * hz * FP64_OPS_PER_SM_CLK / FP64_OPS_PER_VARIATE}
     lim = min(b, key=b.get)
-    return {"unit": "variates/s", "sm_mhz": mhz, "sms": sms, **b, "min": lim,
-            "frac_of_min": variates_per_s / b[lim]}
+    out = {"unit": "variates/s", "sm_mhz": mhz, "sms": sms, **b, "min": lim,
+           "frac_of_min": variates_per_s / b[lim]}
+    # the bound the headline kernel actually meets: instruction issue (4 warp-instructions
+    # per SM clock) at the warp-instruction count ncu measured per launch
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            rec = json.load(f)["c2"]
+        wipv = rec["warp_instructions_per_launch"] / rec["variates_per_launch"]
+        ceiling = sms * hz * 4 / wipv
+        out["issue"] = {"warp_instr_per_variate": wipv, "ceiling": ceiling, "frac": variates_per_s / ceiling,
+                        "source": rec["source"]}
+    except Exception:
+        pass
+    return out
 
 
 def e2e_host(first_id, n_streams, steps, warmup):
