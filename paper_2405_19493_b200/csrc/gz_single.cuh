@@ -338,94 +338,149 @@ struct ZigExit {
 };
 
 /* walk every entry offset 0..SZ_E-1 of chunk blockIdx.x through the chunk (one warp
-   per chunk, lanes 0..SZ_E-1 walk); each walk also leaves the bitmap of its accepted
-   attempt starts (SZ_L bits) in bm, so the emit pass needs no walk */
+   per chunk) and leave, per entry, where the walk leaves the chunk, its accepted
+   count and the bitmap of its accepted attempt starts (SZ_L bits), so the emit pass
+   needs no walk.  The chunk is cut into SZ_S sub-chunks walked at once from every
+   entry (lane = SZ_E * sub-chunk + entry), and the sub-chunk walks are composed per
+   chunk entry by shuffles: the serial chain a lane follows is SZ_L / SZ_S positions
+   long, not SZ_L.  A walk that leaves a sub-chunk SZ_E or more positions past its end
+   (a long tail attempt) has no precomputed continuation: that chunk entry is walked
+   through the whole chunk by one lane instead (same result). */
 constexpr int SZ_W = SZ_L / 32;   /* bitmap words per chunk and entry */
 static_assert(SZ_W == 32, "the emit pass maps one bitmap word per lane");
-constexpr int SZ_CPW = 4;   /* chunks per warp in the exits pass (SZ_E lanes each) */
+constexpr int SZ_S = 32 / SZ_E;   /* sub-chunks per chunk */
+constexpr int SZ_SL = SZ_L / SZ_S;   /* positions per sub-chunk */
+constexpr int SZ_SW = SZ_SL / 32;    /* bitmap words per sub-chunk and entry */
+static_assert(SZ_S * SZ_E == 32 && SZ_SL % 32 == 0, "one lane per (sub-chunk, entry)");
+
+/* walk positions [p, end) of the packed chunk pk from p, setting the accepted starts in
+   the bitmap words bmw[(q - w0) >> 5] (q: chunk position); returns the position where
+   the walk leaves [.., end) and adds the accepted count; bad on a zero-length position */
+__device__ __forceinline__ int zig_walk(const uint16_t* pk, int p, int end, int w0, uint32_t* bmw, int& cnt,
+                                        int& bad)
+{
+    int cw = p >> 5;
+    uint32_t word = 0;   /* bitmap word cw, stored when the walk leaves it */
+    while (p < end) {
+        const uint32_t v = pk[p];
+        const int l = (int)(v & 0x7FFFu);
+        if (l == 0) {
+            bad = 1;
+            break;
+        }
+        const uint32_t acc = v >> 15;
+        cnt += (int)acc;
+        if ((p >> 5) != cw) {
+            bmw[cw - w0] = word;
+            cw = p >> 5;
+            word = 0;
+        }
+        word |= acc << (p & 31);
+        p += l;
+    }
+    if (cw - w0 < (end - (w0 << 5) + 31) >> 5) bmw[cw - w0] = word;
+    return p;
+}
+
 __global__ void __launch_bounds__(32) k_zig_single_exits(const ZigPos* pos, int64_t n_pos, int n_chunks, ZigExit* ex,
                                                          uint32_t* bm)
 {
-    /* padded against bank conflicts: the groups' walks read rows SZ_L + 16 apart, the
-       lanes' bitmap rows are SZ_W + 1 words apart */
-    __shared__ uint16_t s_pk[SZ_CPW][SZ_L + 16];   /* len | acc << 15 */
-    __shared__ uint32_t s_bm[SZ_CPW][SZ_E][SZ_W + 1];
+    __shared__ uint16_t s_pk[SZ_L + 16];
+    __shared__ uint32_t s_sb[SZ_S][SZ_E][SZ_SW + 1];   /* sub-chunk bitmaps */
+    __shared__ uint32_t s_out[SZ_E][SZ_W + 1];         /* chunk bitmaps per entry */
     const int lane = threadIdx.x;
-    for (int g = 0; g < SZ_CPW; ++g) {
-        const int c = blockIdx.x * SZ_CPW + g;
-        if (c >= n_chunks) break;
-        const int64_t c0 = (int64_t)c * SZ_L;
-        const int nl = (int)(n_pos - c0 < SZ_L ? n_pos - c0 : SZ_L);
-        if (nl == SZ_L) {
-            /* 16-byte loads: four positions per lane and step */
-            const uint4* src = reinterpret_cast<const uint4*>(pos + c0);
+    const int c = blockIdx.x;
+    if (c >= n_chunks) return;
+    const int64_t c0 = (int64_t)c * SZ_L;
+    const int nl = (int)(n_pos - c0 < SZ_L ? n_pos - c0 : SZ_L);
+    if (nl == SZ_L) {
+        /* 16-byte loads: four positions per lane and step */
+        const uint4* src = reinterpret_cast<const uint4*>(pos + c0);
 #pragma unroll
-            for (int it = 0; it < SZ_L / 4 / 32; ++it) {
-                const int q = it * 32 + lane;
-                const uint4 v = src[q];
-                const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+        for (int it = 0; it < SZ_L / 4 / 32; ++it) {
+            const int q = it * 32 + lane;
+            const uint4 v = src[q];
+            const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const uint32_t len = w[k] & 0xFFFFu, acc = (w[k] >> 16) & 0xFFu;
-                    s_pk[g][4 * q + k] = (uint16_t)(len > 0x7FFFu ? 0u : (len | (acc ? 0x8000u : 0u)));
-                }
-            }
-        } else {
-            for (int i = lane; i < nl; i += 32) {
-                const ZigPos zp = pos[c0 + i];
-                s_pk[g][i] = (uint16_t)(zp.len > 0x7FFF ? 0 : (zp.len | (zp.acc ? 0x8000 : 0)));
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t len = w[k] & 0xFFFFu, acc = (w[k] >> 16) & 0xFFu;
+                s_pk[4 * q + k] = (uint16_t)(len > 0x7FFFu ? 0u : (len | (acc ? 0x8000u : 0u)));
             }
         }
-#pragma unroll
-        for (int e = 0; e < SZ_E; ++e) s_bm[g][e][lane] = 0u;
+    } else {
+        for (int i = lane; i < nl; i += 32) {
+            const ZigPos zp = pos[c0 + i];
+            s_pk[i] = (uint16_t)(zp.len > 0x7FFF ? 0 : (zp.len | (zp.acc ? 0x8000 : 0)));
+        }
+    }
+    {
+        uint32_t* sb = &s_sb[0][0][0];
+        for (int i = lane; i < SZ_S * SZ_E * (SZ_SW + 1); i += 32) sb[i] = 0u;
+        uint32_t* so = &s_out[0][0];
+        for (int i = lane; i < SZ_E * (SZ_W + 1); i += 32) so[i] = 0u;
     }
     __syncwarp();
-    /* lane = SZ_E * g + e walks entry e of chunk g */
+    /* lane = SZ_E * g + e walks entry e of sub-chunk g */
     const int g = lane / SZ_E, e = lane % SZ_E;
-    const int c = blockIdx.x * SZ_CPW + g;
-    if (c < n_chunks) {
-        const int64_t c0 = (int64_t)c * SZ_L;
-        const int nl = (int)(n_pos - c0 < SZ_L ? n_pos - c0 : SZ_L);
-        const uint16_t* pk = s_pk[g];
-        uint32_t* bmw = s_bm[g][e];
-        int p = e, cnt = 0, bad = 0, cw = 0;
-        uint32_t word = 0;   /* bitmap word cw, stored when the walk leaves it */
-        while (p < nl) {
-            const uint32_t v = pk[p];
-            const int l = (int)(v & 0x7FFFu);
-            if (l == 0) {
-                bad = 1;
-                break;
-            }
-            const uint32_t acc = v >> 15;
-            cnt += (int)acc;
-            if ((p >> 5) != cw) {
-                bmw[cw] = word;
-                cw = p >> 5;
-                word = 0;
-            }
-            word |= acc << (p & 31);
-            p += l;
-        }
-        bmw[cw] = word;
-        ZigExit x;
-        x.exit = bad ? 0 : p - nl;
-        x.cnt = cnt;
-        x.bad = bad;
-        x.pad = 0;
-        ex[(int64_t)c * SZ_E + e] = x;
+    const int sbeg = g * SZ_SL;
+    const int send = min(sbeg + SZ_SL, nl);
+    int cnt = 0, bad = 0, xo = 0;
+    if (sbeg < nl) {
+        const int p = zig_walk(s_pk, sbeg + e, send, sbeg >> 5, s_sb[g][e], cnt, bad);
+        xo = bad ? 0 : p - send;
     }
     __syncwarp();
-    for (int g2 = 0; g2 < SZ_CPW; ++g2) {
-        const int c2 = blockIdx.x * SZ_CPW + g2;
-        if (c2 >= n_chunks) break;
-        uint32_t* dst = bm + (int64_t)c2 * SZ_E * SZ_W;
+    /* compose the sub-chunk walks for chunk entry e = lane (lanes >= SZ_E follow along) */
+    int en = lane < SZ_E ? lane : 0, tot = 0, cbad = 0, slow = 0;
+    int ent[SZ_S];
 #pragma unroll
-        for (int e2 = 0; e2 < SZ_E; ++e2) dst[e2 * SZ_W + lane] = s_bm[g2][e2][lane];
+    for (int gg = 0; gg < SZ_S; ++gg) {
+        ent[gg] = en;
+        const int src = SZ_E * gg + (en < SZ_E ? en : 0);
+        const int x_ = __shfl_sync(GZ_FULL, xo, src);
+        const int c_ = __shfl_sync(GZ_FULL, cnt, src);
+        const int b_ = __shfl_sync(GZ_FULL, bad, src);
+        if (gg * SZ_SL < nl && !slow && !cbad) {
+            if (en >= SZ_E) {
+                slow = 1;          /* overhang past the precomputed entries */
+            } else {
+                tot += c_;
+                cbad |= b_;
+                en = x_;
+            }
+        }
     }
+    if (lane < SZ_E) {
+        ZigExit x;
+        if (slow) {
+            /* the whole chunk from entry `lane` by this lane */
+            int sc = 0, sbd = 0;
+            const int p = zig_walk(s_pk, lane, nl, 0, s_out[lane], sc, sbd);
+            x.exit = sbd ? 0 : p - nl;
+            x.cnt = sc;
+            x.bad = sbd;
+        } else {
+#pragma unroll
+            for (int gg = 0; gg < SZ_S; ++gg) {
+                if (gg * SZ_SL >= nl || cbad) break;
+#pragma unroll
+                for (int w = 0; w < SZ_SW; ++w) s_out[lane][gg * SZ_SW + w] = s_sb[gg][ent[gg]][w];
+            }
+            x.exit = cbad ? 0 : en;
+            x.cnt = tot;
+            x.bad = cbad;
+        }
+        x.pad = 0;
+        ex[(int64_t)c * SZ_E + lane] = x;
+    }
+    __syncwarp();
+    uint32_t* dst = bm + (int64_t)c * SZ_E * SZ_W;
+#pragma unroll
+    for (int e2 = 0; e2 < SZ_E; ++e2) dst[e2 * SZ_W + lane] = s_out[e2][lane];
 }
 
-/* the chunk chain, three levels: LINK_B chunks per block composed for every entry,
+/* the chunk chain, three levels: lb <= LINK_B chunks per block composed for every entry
+   (the host picks lb near sqrt(chunks): both serial chains stay short),
    blocks linked by one thread, chunk entries/bases expanded per block */
 constexpr int LINK_B = 128;
 
@@ -434,11 +489,11 @@ struct ZigLinkF {
     int64_t cnt;
 };
 
-__global__ void __launch_bounds__(32) k_zig_single_link_blocks(const ZigExit* ex, int n_chunks, ZigLinkF* fb)
+__global__ void __launch_bounds__(32) k_zig_single_link_blocks(const ZigExit* ex, int n_chunks, int lb, ZigLinkF* fb)
 {
     __shared__ ZigExit s_ex[LINK_B * SZ_E];
     const int b = blockIdx.x;
-    const int c0 = b * LINK_B, c1 = min(c0 + LINK_B, n_chunks);
+    const int c0 = b * lb, c1 = min(c0 + lb, n_chunks);
     for (int i = threadIdx.x; i < (c1 - c0) * SZ_E; i += 32) s_ex[i] = ex[(int64_t)c0 * SZ_E + i];
     __syncwarp();
     const int e0 = threadIdx.x;
@@ -495,12 +550,13 @@ __global__ void __launch_bounds__(256) k_zig_single_link_top(const ZigLinkF* fb,
     top->bad = bad;
 }
 
-__global__ void __launch_bounds__(32) k_zig_single_link_expand(const ZigExit* ex, int n_chunks, const int* b_entry,
-                                                               const int64_t* b_base, int* entry, int64_t* base)
+__global__ void __launch_bounds__(32) k_zig_single_link_expand(const ZigExit* ex, int n_chunks, int lb,
+                                                               const int* b_entry, const int64_t* b_base, int* entry,
+                                                               int64_t* base)
 {
     __shared__ ZigExit s_ex[LINK_B * SZ_E];
     const int b = blockIdx.x;
-    const int c0 = b * LINK_B, c1 = min(c0 + LINK_B, n_chunks);
+    const int c0 = b * lb, c1 = min(c0 + lb, n_chunks);
     for (int i = threadIdx.x; i < (c1 - c0) * SZ_E; i += 32) s_ex[i] = ex[(int64_t)c0 * SZ_E + i];
     __syncwarp();
     if (threadIdx.x != 0) return;
