@@ -597,7 +597,24 @@ __global__ void __launch_bounds__(32) k_zig_single_emit(const ZigPos* pos, const
     if (b0 >= o.need || e < 0 || top->bad) return;
     const int64_t c0 = (int64_t)c * SZ_L;
     const int lane = threadIdx.x;
-    uint32_t word = bm[((int64_t)c * SZ_E + e) * SZ_W + lane];
+    const int nl = (int)(n_pos - c0 < SZ_L ? n_pos - c0 : SZ_L);
+    /* the chunk's values staged in shared memory by coalesced loads (one double of
+       padding per 32: a lane's run of 32 positions starts in its own bank pair) */
+    __shared__ double s_v[SZ_L + SZ_L / 32];
+    __shared__ double s_o[SZ_L];
+    if (nl == SZ_L) {
+        const double2* src = reinterpret_cast<const double2*>(val + c0);
+#pragma unroll 4
+        for (int it = 0; it < SZ_L / 64; ++it) {
+            const int q = it * 32 + lane;
+            const double2 v = src[q];
+            s_v[2 * q + (q >> 4)] = v.x;
+            s_v[2 * q + 1 + (q >> 4)] = v.y;
+        }
+    } else {
+        for (int i = lane; i < nl; i += 32) s_v[i + (i >> 5)] = val[c0 + i];
+    }
+    const uint32_t word = bm[((int64_t)c * SZ_E + e) * SZ_W + lane];
     const int mine = __popc(word);
     int incl = mine;
 #pragma unroll
@@ -605,21 +622,35 @@ __global__ void __launch_bounds__(32) k_zig_single_emit(const ZigPos* pos, const
         const int v = __shfl_up_sync(GZ_FULL, incl, off);
         if (lane >= off) incl += v;
     }
-    int64_t rank = b0 + incl - mine;
-    while (word && rank < o.need) {
-        const int bit = __ffs(word) - 1;
-        word &= word - 1;
-        const int64_t p = c0 + 32 * lane + bit;
-        o.out[rank] = val[p];
-        if (rank == o.need - 1) {
-            /* the segment's last needed deviate: the stream continues after it */
-            const uint64_t s0 = st0[0];
-            const uint64_t gam = SRC == 1 ? st0[1] : 0;
-            const uint64_t draws = (uint64_t)(o.p0 + p + pos[p].len);
-            o.state_out[0] = single_state_at<SRC>(s0, gam, draws);
-            if (SRC == 1) o.state_out[1] = gam;
+    const int r0 = incl - mine;                      /* rank of this lane's first value in the chunk */
+    const int cnt = __shfl_sync(GZ_FULL, incl, 31);
+    __syncwarp();
+    /* compact the accepted starts' values in order */
+    {
+        uint32_t w = word;
+        int r = r0;
+        const double* sv = s_v + 33 * lane;
+        while (w) {
+            const int bit = __ffs(w) - 1;
+            w &= w - 1;
+            s_o[r++] = sv[bit];
         }
-        ++rank;
+    }
+    __syncwarp();
+    const int lim = (int)(o.need - b0 < (int64_t)cnt ? o.need - b0 : (int64_t)cnt);
+    double* const dst = o.out + b0;
+    for (int i = lane; i < lim; i += 32) dst[i] = s_o[i];
+    /* the segment's last needed deviate: the stream continues after it */
+    const int64_t k = o.need - 1 - b0;           /* its rank in this chunk */
+    if (k >= r0 && k < r0 + mine) {
+        uint32_t w = word;
+        for (int t = 0; t < (int)(k - r0); ++t) w &= w - 1;
+        const int64_t p = c0 + 32 * lane + (__ffs(w) - 1);
+        const uint64_t s0 = st0[0];
+        const uint64_t gam = SRC == 1 ? st0[1] : 0;
+        const uint64_t draws = (uint64_t)(o.p0 + p + pos[p].len);
+        o.state_out[0] = single_state_at<SRC>(s0, gam, draws);
+        if (SRC == 1) o.state_out[1] = gam;
     }
 }
 
