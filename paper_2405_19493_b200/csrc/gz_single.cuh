@@ -31,6 +31,8 @@
 constexpr int64_t SINGLE_MIN_N = 1 << 15;       /* below this the warp kernel is faster */
 constexpr int64_t SINGLE_MIN_GUARD = 1 << 13;   /* a guard trip needs a whole rejected chunk */
 constexpr int SP_T = 256;                       /* polar: attempts per block */
+constexpr int CL_J = 8;                         /* ziggurat classify: positions per thread */
+constexpr uint64_t CL_A512 = 0x94fba1cf4801ULL, CL_C512 = 0x9e1922a97200ULL;   /* 512 LCG steps */
 constexpr int SZ_L = 1024;                      /* ziggurat: draw positions per chunk (= 32 bitmap words) */
 constexpr int SZ_E = 8;                         /* ziggurat: entry offsets walked per chunk */
 
@@ -266,67 +268,76 @@ struct ZigPos {
 
 template <int SRC, bool MOD>
 __global__ void __launch_bounds__(256) k_zig_single_classify(const uint64_t* st0, int64_t p0, int64_t n_pos,
-                                                             const ulonglong2* kw, const double2* yd, int n_layers,
-                                                             double r, int64_t guard, ZigPos* pos, double* val)
+                                                             const ulonglong2* kw, const double2* yd, const float2* yf,
+                                                             int n_layers, double r, int64_t guard, ZigPos* pos,
+                                                             double* val)
 {
     __shared__ uint64_t s_base;
-    const int64_t pb = p0 + (int64_t)blockIdx.x * 256;
+    /* a block classifies CL_J * 256 positions: thread t takes pb + t + 256 j, j < CL_J,
+       so the per-thread jump is paid once and the next position is a constant jump of
+       512 LCG steps (coalesced stores at every j) */
+    const int64_t pb = p0 + (int64_t)blockIdx.x * (256 * CL_J);
     const int t = threadIdx.x;
     uint64_t s0 = st0[0], gam = 0;
     if constexpr (SRC == 1) gam = st0[1];
-    uint64_t S;   /* the state before position pb + t's draw */
+    uint64_t St;   /* the state before position pb + t + 256 j's draw */
     if constexpr (SRC == 0) {
         if (t == 0) s_base = single_state_at<0>(s0, 0, (uint64_t)pb);
         __syncthreads();
         uint64_t A, C;
         lcg_jump_n(2 * (uint64_t)t, A, C);
-        S = (A * s_base + C) & GZ_MASK48;
+        St = (A * s_base + C) & GZ_MASK48;
     } else {
-        S = s0 + (uint64_t)(pb + t) * gam;
+        St = s0 + (uint64_t)(pb + t) * gam;
     }
-    const int64_t k = pb + t;
-    if (k >= p0 + n_pos) return;
     int ib = 0;
     while ((1 << (ib + 1)) <= n_layers) ++ib;
     const uint32_t imask = (uint32_t)n_layers - 1u;
     const int mbits = 63 - ib;
     const uint64_t mmask = (1ULL << mbits) - 1ULL;
-    /* ZigguratSampler._draw one attempt (samplers.py:95-115 / 144-165) */
-    const uint64_t u = gz_next_seq<SRC>(S, gam);
-    uint32_t i;
-    uint64_t m;
-    bool neg;
-    if constexpr (MOD) {
-        i = (uint32_t)u & imask;
-        m = u >> (ib + 1);
-        neg = (u >> ib) & 1;
-    } else {
-        i = (uint32_t)(u >> mbits) & imask;
-        m = u & mmask;
-        neg = u >> 63;
-    }
-    const ulonglong2 kk = kw[i];
-    double x = __dmul_rn(__ull2double_rn(m), __longlong_as_double((long long)kk.y));
-    ZigPos zp{1, 1, 0};
-    if (m >= kk.x) {
-        if (i != 0) {
-            const uint64_t u2 = gz_next_seq<SRC>(S, gam);
-            const double y = __dadd_rn(yd[i].x, __dmul_rn(gz_unit53(u2), yd[i].y));
-            zp.len = 2;
-            zp.acc = wedge_exact(y, __dmul_rn(__dmul_rn(-0.5, x), x)) ? 1 : 0;
+    for (int jj = 0; jj < CL_J; ++jj) {
+        const int64_t k = pb + t + 256 * jj;
+        if (k >= p0 + n_pos) break;
+        uint64_t S = St;
+        if constexpr (SRC == 0) St = (CL_A512 * St + CL_C512) & GZ_MASK48;
+        else St += 256 * gam;
+        /* ZigguratSampler._draw one attempt (samplers.py:95-115 / 144-165) */
+        const uint64_t u = gz_next_seq<SRC>(S, gam);
+        uint32_t i;
+        uint64_t m;
+        bool neg;
+        if constexpr (MOD) {
+            i = (uint32_t)u & imask;
+            m = u >> (ib + 1);
+            neg = (u >> ib) & 1;
         } else {
-            const TailOut to = tail_seq<SRC>(S, gam, r, guard);
-            if (to.k < 0 || 1 + 2 * (int64_t)to.k > 65535) {
-                zp.len = 0;   /* guard tripped or an overlong tail: the caller falls back */
-                zp.acc = 0;
+            i = (uint32_t)(u >> mbits) & imask;
+            m = u & mmask;
+            neg = u >> 63;
+        }
+        const ulonglong2 kk = kw[i];
+        double x = __dmul_rn(__ull2double_rn(m), __longlong_as_double((long long)kk.y));
+        ZigPos zp{1, 1, 0};
+        if (m >= kk.x) {
+            if (i != 0) {
+                const uint64_t u2 = gz_next_seq<SRC>(S, gam);
+                zp.len = 2;
+                /* the float pre-filter settles all but the cases within 2^-15 of the boundary */
+                zp.acc = wedge_accept_f(u2, x, yd + i, yf[i]) ? 1 : 0;
             } else {
-                zp.len = (uint16_t)(1 + 2 * to.k);
-                x = to.v;
+                const TailOut to = tail_seq<SRC>(S, gam, r, guard);
+                if (to.k < 0 || 1 + 2 * (int64_t)to.k > 65535) {
+                    zp.len = 0;   /* guard tripped or an overlong tail: the caller falls back */
+                    zp.acc = 0;
+                } else {
+                    zp.len = (uint16_t)(1 + 2 * to.k);
+                    x = to.v;
+                }
             }
         }
+        pos[k - p0] = zp;
+        val[k - p0] = neg ? -x : x;
     }
-    pos[k - p0] = zp;
-    val[k - p0] = neg ? -x : x;
 }
 
 /* per chunk and entry offset e: where the walk leaves the chunk and what it found */
