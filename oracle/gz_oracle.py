@@ -47,6 +47,8 @@ def lib():
         L.gzo_build_tables.argtypes = [ctypes.c_int, ctypes.POINTER(GzoTables)]
         L.gzo_fill_gaussians.argtypes = [ctypes.c_int, ctypes.c_int, P, i64, i64, i64, P, P, P, P, P, P, P,
                                          i64, ctypes.c_int]
+        L.gzo_fill_digest.argtypes = [ctypes.c_int, ctypes.c_int, P, i64, i64, P, P, P, P, P, P, P, P, i64,
+                                      ctypes.c_int]
         L.gzo_fill_u64.argtypes = [ctypes.c_int, i64, i64, i64, P, P, P]
         L.gzo_occupancy.argtypes = [ctypes.c_int, ctypes.c_int, P, P, P, i64, P, P, i64]
         L.gzo_tail_sample.argtypes = [ctypes.c_int, P, P, ctypes.c_double, i64, P]
@@ -123,6 +125,37 @@ def fill_gaussians(alg, source, states, n_per, spare=None, has=None, layers=None
                                       n_per, n_per, _p(states), _p(st_out), _p(spare), _p(has),
                                       _p(spare_out), _p(has_out), _p(out), guard, nthreads)
     return out, st_out, spare_out, has_out, status
+
+
+def fill_digest(alg, source, states, n_per, spare=None, has=None, layers=None, guard=GUARD, nthreads=0,
+                psum=False):
+    """fill_gaussians without the output buffer (full-size parity checks).
+    Returns (digest uint64[n, 3], states_out, spare_out, has_out, psum f64[n, 4] or None, status);
+    digest = (xor of bit patterns, sum (j+1)*(bits>>32), sum (j+1)*(bits & 0xffffffff)) mod 2^64."""
+    states = np.ascontiguousarray(states, dtype=np.uint64)
+    n = states.shape[0]
+    dig = np.zeros((n, 3), dtype=np.uint64)
+    st_out = np.empty_like(states)
+    t = None if alg == "polar" else tables(layers or default_layers(alg))
+    spare_out = np.zeros(n) if alg == "polar" else None
+    has_out = np.zeros(n, dtype=np.uint8) if alg == "polar" else None
+    ps = np.zeros((n, 4)) if psum else None
+    if spare is not None:
+        spare = np.ascontiguousarray(spare, dtype=np.float64)
+        has = np.ascontiguousarray(has, dtype=np.uint8)
+    status = lib().gzo_fill_digest(ALG[alg], SRC[source], None if t is None else ctypes.byref(t.raw), n, n_per,
+                                   _p(states), _p(st_out), _p(spare), _p(has), _p(spare_out), _p(has_out),
+                                   _p(dig), _p(ps), guard, nthreads)
+    return dig, st_out, spare_out, has_out, ps, status
+
+
+def digest_rows(rows):
+    """The fill_digest witnesses of materialised rows (numpy float64 [n, n_per])."""
+    b = np.ascontiguousarray(rows, dtype=np.float64).view(np.uint64)
+    w = np.arange(1, b.shape[1] + 1, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        return np.stack([np.bitwise_xor.reduce(b, axis=1), ((b >> np.uint64(32)) * w).sum(1, dtype=np.uint64),
+                         ((b & np.uint64(0xffffffff)) * w).sum(1, dtype=np.uint64)], 1)
 
 
 def occupancy(alg, source, state_words, n_calls, layers=None, guard=GUARD):
@@ -225,6 +258,33 @@ def lcg_state(seed):
 
 def sm_output_seed(master, i):
     return mix64((master + (i + 1) * GOLDEN_GAMMA) & MASK64)
+
+
+def mix64_np(z):
+    """sources.py:83-87 over a uint64 array (wrapping arithmetic)."""
+    z = np.asarray(z, dtype=np.uint64).copy()
+    with np.errstate(over="ignore"):
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+    return z ^ (z >> np.uint64(31))
+
+
+def config_states_range(cfg, first, count):
+    """config_states(cfg, range(first, first + count)), vectorised (large shards)."""
+    ids = np.arange(first, first + count, dtype=np.uint64)
+    g = np.uint64(GOLDEN_GAMMA)
+    with np.errstate(over="ignore"):
+        if cfg in ("c2", "c4"):
+            base = np.uint64(7 if cfg == "c2" else 99)
+            return ((base + ids) ^ np.uint64(0x5DEECE66D)) & np.uint64((1 << 48) - 1)
+        if cfg in ("c1", "c3"):
+            m = np.uint64(42 if cfg == "c1" else 1234)
+            s = mix64_np(m + (ids + np.uint64(1)) * g)
+        elif cfg == "c5":
+            s = ids ^ np.uint64(0xC0FFEE)
+        else:
+            raise ValueError(cfg)
+    return np.stack([s, np.full_like(s, g)], 1)
 
 
 def config_states(cfg, ids):

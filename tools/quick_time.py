@@ -24,6 +24,8 @@ def t5(reps=5, gens=10):
 def t(cfg, n=None, reps=10):
     if cfg == "c5":
         return t5()
+    checks = cfg.endswith("s")
+    cfg = cfg.rstrip("s")
     c = streams.CONFIGS[cfg]
     n = n or c.n_streams
     st0 = streams.config_states(cfg, 0, n)
@@ -31,6 +33,9 @@ def t(cfg, n=None, reps=10):
     kw = {}
     if c.sampler == "polar":
         kw = dict(spare=torch.zeros(n, dtype=torch.float64, device="cuda"), has_spare=torch.zeros(n, dtype=torch.uint8, device="cuda"))
+    if checks:
+        kw["checksum"] = torch.zeros(n, dtype=torch.int64, device="cuda")
+        kw["psum"] = torch.zeros((n, 4), dtype=torch.float64, device="cuda")
     for _ in range(3):
         st = st0.clone(); streams.fill_gaussians_streams(c.sampler, c.source, st, out, sync=False, **kw)
     torch.cuda.synchronize()
@@ -42,7 +47,7 @@ def t(cfg, n=None, reps=10):
     e1.record(); torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / reps
     nv = n * c.n_per
-    print(f"{cfg}: {n}x{c.n_per} {ms:.3f} ms  {nv/ms/1e6:.1f} Gvar/s  {nv*8/ms/1e6:.0f} GB/s", flush=True)
+    print(f"{cfg}{'+stats' if checks else ''}: {n}x{c.n_per} {ms:.3f} ms  {nv/ms/1e6:.1f} Gvar/s  {nv*8/ms/1e6:.0f} GB/s", flush=True)
 
 pol = os.environ.get("GZ_POLICY", "auto")
 streams.set_kernel_policy(pol)
