@@ -3,30 +3,43 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-Headline workload = BASELINE.json configs[1] (config 2): the polar method over
-the 48-bit Java LCG, 2^20 independent streams seeded Lcg48(7 + stream id), 256
-fp64 variates per stream per step, per GPU (weak scaling: rank r owns stream
-ids [r*2^20, (r+1)*2^20)).  One step = every stream emits its next 256 variates
-(the streams continue from step to step).  The output (2 GiB per GPU) is
-larger than L2, so no flush is needed between steps.
+Headline workload = BASELINE.json configs[3] (config 4), the largest
+single-GPU configuration: the original ziggurat (128 layers) over the 48-bit
+Java LCG, 2^22 independent streams x 256 fp64 variates per GPU per step,
+stream gid seeded Lcg48(99 + gid), GPU g owning gids [g*2^22, (g+1)*2^22)
+(weak scaling), with the per-stream xor checksums and power sums fused into
+the fill and the global mean/variance/kurtosis merged across ranks.  One step =
+every stream emits its next 256 variates (the streams continue from step to
+step).  The output (8 GiB per GPU per step) is far larger than L2, so no flush
+is needed between steps.
 
-value   = variates/s over all ranks (device time, CUDA events, max over ranks)
-e2e     = the same work through the reference-facing host-buffer C-ABI call
-          (gz_fill_gaussians_host): stream states in from pinned host memory,
-          deviates and states back to pinned host memory, every step.
-roofline= HBM-store bound of the fill kernel (8 B per variate) against the
-          measured copy bandwidth of MEASURED_PEAKS.json.
-cpu_baseline = the CPU oracle port (oracle/gz_oracle.c, OpenMP over streams)
-          on a bounded sample of the same workload, rank 0, N=1 only.
-Also reported under "configs": the other four BASELINE configs (device time).
+value    = variates/s over all ranks (device time, CUDA events on the launching
+           stream, max over ranks); one kernel (k_zig_tma) per step.
+e2e      = the same work through the reference-facing host-buffer C-ABI call
+           (gz_fill_gaussians_host): stream states in from pinned host memory,
+           deviates, states and checksums back to pinned host memory, every step.
+roofline = the fill kernel's algorithmic bytes (8 B stored per variate) per
+           launch / its launch time, against the measured copy bandwidth of
+           MEASURED_PEAKS.json; traffic = DRAM bytes per launch from the
+           committed `ncu --set full` capture (profiles/traffic.json).
+cpu_baseline = the CPU oracle port (oracle/gz_oracle.c, OpenMP over streams) on
+           a bounded sample of the same workload, rank 0, N=1 only, plus the
+           reference's own numba engine ("reference as-is", baseline/_ref) on
+           P worker processes when it is installed.
+configs  = the other four BASELINE configs (device time).
 
---impl reference: the reference algorithm's CPU implementation (the oracle
-port; the Python reference cannot travel to the GPU box) on all host threads,
-same metric and config, one bounded sample per step.
+--gpus N without a torchrun environment re-launches this script under
+torch.distributed.run with N ranks (one per GPU, NCCL), rendezvous on 127.0.0.1.
+
+--impl reference: the reference algorithm's CPU implementation (the oracle port;
+the Python/numba reference is compiled nowhere, and /root/reference is absent
+on the GPU box) on all host threads, same metric and config, one bounded sample
+of the workload per step; rank 0 only.
 """
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -36,31 +49,44 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-STREAMS_PER_GPU = 1 << 20
+HEAD = "c4"
+STREAMS_PER_GPU = 1 << 22
 N_PER = 256
-METRIC = "fp64 Gaussian variates/sec (polar x LCG48, config 2)"
+METRIC = "fp64 Gaussian variates/sec (ziggurat x LCG48, config 4, fused per-stream checksums + moments)"
 UNIT = "variates/s"
-REF_SAMPLE_STREAMS = 1 << 17     # CPU sample per step: 2^17 streams x 256 = 33.5M variates
+WORKLOAD = "config 4: original ziggurat (128 layers) x LCG48, 2^22 streams x 256 variates per GPU per step, " \
+           "fused per-stream xor checksums + power sums, global moments merged over ranks"
+REF_SAMPLE_STREAMS = 1 << 20     # CPU sample per step: 2^20 streams x 256 = 2^28 variates of config 4
+NUMBA_SAMPLE_STREAMS = 1 << 14   # reference-as-is sample: 2^14 streams x 256, one engine call per stream
 
 
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             d = json.load(f)
-        return float(d["hbm_gbs"]), "measured"
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy read+write)"
     except Exception:
-        return 6650.0, "fallback"
+        return 6650.0, "fallback (B200_PROFILING.md)"
 
 
 def traffic_record(cfg):
-    """dram read + write bytes per launch of the headline kernel, from the committed
-    `ncu --set full` capture (profiles/traffic.json), or None."""
+    """ncu record of the config's fill kernel (profiles/traffic.json), or None."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            rec = json.load(f).get(cfg)
-        return None if rec is None else rec["bytes_per_launch"]
+            return json.load(f).get(cfg)
     except Exception:
         return None
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
 
 
 class ClockSampler:
@@ -107,12 +133,31 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(sm)}
 
 
+# ---------------------------------------------------------------- process plumbing
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def spawn_ranks(args):
+    """Re-launch under torch.distributed.run with args.gpus ranks; rank 0 prints the line."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd).returncode
+
+
 def dist_setup(n_gpus):
     import torch
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != n_gpus:
+        raise SystemExit(f"bench.py: --gpus {n_gpus} but WORLD_SIZE={world}")
     if world > 1:
         import torch.distributed as dist
 
@@ -145,8 +190,11 @@ def barrier(world):
         torch.cuda.synchronize()
 
 
+# ---------------------------------------------------------------- device timing
+
 def time_fill(cfg, first_id, n_streams, steps, warmup, world, checks=False):
-    """Device-timed steps of one config's fill on this rank.  Returns dict."""
+    """Device-timed steps of one config's fill on this rank (CUDA events on the
+    stream the kernels are launched on)."""
     import torch
 
     from paper_2405_19493_b200 import streams
@@ -162,15 +210,17 @@ def time_fill(cfg, first_id, n_streams, steps, warmup, world, checks=False):
     if checks:
         ck = torch.zeros(n_streams, dtype=torch.int64, device="cuda")
         ps = torch.zeros((n_streams, 4), dtype=torch.float64, device="cuda")
+    stream = torch.cuda.current_stream()
     for _ in range(warmup):
         streams.fill_gaussians_streams(c.sampler, c.source, st, out, checksum=ck, psum=ps, sync=False, **kw)
     streams.engine_check()
     barrier(world)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
+    e0.record(stream)
     for _ in range(steps):
-        streams.fill_gaussians_streams(c.sampler, c.source, st, out, checksum=ck, psum=ps, sync=False, **kw)
-    e1.record()
+        streams.fill_gaussians_streams(c.sampler, c.source, st, out, checksum=ck, psum=ps, sync=False,
+                                       stream=stream, **kw)
+    e1.record(stream)
     e1.synchronize()
     streams.engine_check()
     ms = e0.elapsed_time(e1) / steps
@@ -204,18 +254,15 @@ def time_mutate(first_ind, n_ind, generations, steps, warmup, world):
             "launches": steps}
 
 
-# the polar x LCG48 path is bounded by HBM stores (8 B/variate), the
-# integer pipe and (for polar) the FP64 pipe.  Algorithmic operations per variate:
-#   int : 1.2725 u64/variate x ~10 SASS int ops per LCG48 u64 (2 x mul-add + shifts)
-#         + ~10 for extraction / compare / conversion                      = 22.7
-#   fp64: per attempt (0.6363/variate) 2 x (int->f64, 2u-1) + s (3) + 2 compares = 9;
-#         per pair (0.5/variate) glibc log table path 15, -2*log 1, divide 8,
-#         square root 9, the two products 2                                 = 35
-#         -> 0.6363 * 9 + 0.5 * 35                                          = 23.2
-# Pipe rates per SM per clock: int32 64 (CUDA throughput table, cc 10.0); FP64 62
-# (measured, tools/calib/calib_pipes.cu).  Clock: the median sampled under load.
-INT_OPS_PER_VARIATE = 22.7
-FP64_OPS_PER_VARIATE = 23.2
+# config 4 is bounded by HBM stores (8 B per variate) or the integer
+# pipe.  Algorithmic operations per variate: 1.041 LCG48 u64 draws x ~10 SASS integer
+# ops (two 48-bit multiply-adds on 32-bit halves + shifts) + ~10 for the layer
+# extraction, the 56-bit compare and the address = 20.4 int ops at 64 int32 ops per
+# SM per clock; FP64: the int->f64 product and the fused witnesses (square, two adds,
+# two FMAs) = 6 ops at 62 per SM per clock (measured, tools/calib/calib_pipes.cu).
+# Clock: the median sampled under load.
+INT_OPS_PER_VARIATE = 1.041 * 10 + 10
+FP64_OPS_PER_VARIATE = 6.0
 INT_OPS_PER_SM_CLK = 64
 FP64_OPS_PER_SM_CLK = 62
 
@@ -229,31 +276,23 @@ def compute_bounds(variates_per_s, hbm_gbs, clocks):
     b = {"hbm": hbm_gbs * 1e9 / 8, "int": sms * hz * INT_OPS_PER_SM_CLK / INT_OPS_PER_VARIATE,
          "fp64": sms * hz * FP64_OPS_PER_SM_CLK / FP64_OPS_PER_VARIATE}
     lim = min(b, key=b.get)
-    out = {"unit": "variates/s", "sm_mhz": mhz, "sms": sms, **b, "min": lim,
-           "frac_of_min": variates_per_s / b[lim]}
-    # the bound the headline kernel actually meets: instruction issue (4 warp-instructions
-    # per SM clock) at the warp-instruction count ncu measured per launch
-    try:
-        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            rec = json.load(f)["c2"]
-        wipv = rec["warp_instructions_per_launch"] / rec["variates_per_launch"]
-        ceiling = sms * hz * 4 / wipv
-        out["issue"] = {"warp_instr_per_variate": wipv, "ceiling": ceiling, "frac": variates_per_s / ceiling,
-                        "source": rec["source"]}
-    except Exception:
-        pass
-    return out
+    return {"unit": "variates/s", "sm_mhz": mhz, "sms": sms, **b, "min": lim, "frac_of_min": variates_per_s / b[lim]}
 
+
+# ---------------------------------------------------------------- end to end
 
 def e2e_host(first_id, n_streams, steps, warmup):
-    """Reference-facing path: host buffers through gz_fill_gaussians_host."""
+    """Reference-facing path: host buffers through gz_fill_gaussians_host (the C ABI a
+    numpy caller binds), config 4 with per-stream checksums."""
     import ctypes
 
     import numpy as np
 
-    from paper_2405_19493_b200 import _lib
+    from paper_2405_19493_b200 import _lib, engine
+    from paper_2405_19493_b200.samplers import _default_tables
 
     L = _lib.load()
+    slot = engine.table_slot(_default_tables(128))
     pin = []
 
     def pinned(nbytes):
@@ -263,16 +302,16 @@ def e2e_host(first_id, n_streams, steps, warmup):
         return p
 
     n_out = n_streams * N_PER
-    p_out, p_st_in, p_st_out = pinned(n_out * 8), pinned(n_streams * 8), pinned(n_streams * 8)
-    p_sp, p_hs = pinned(n_streams * 8), pinned(n_streams)
+    p_out, p_st_in, p_st_out, p_ck = pinned(n_out * 8), pinned(n_streams * 8), pinned(n_streams * 8), \
+        pinned(n_streams * 8)
     st_in = np.frombuffer((ctypes.c_uint64 * n_streams).from_address(p_st_in.value), dtype=np.uint64)
     st_out = np.frombuffer((ctypes.c_uint64 * n_streams).from_address(p_st_out.value), dtype=np.uint64)
     ids = np.arange(first_id, first_id + n_streams, dtype=np.uint64)
-    st_in[:] = ((np.uint64(7) + ids) ^ np.uint64(0x5DEECE66D)) & np.uint64((1 << 48) - 1)
+    st_in[:] = ((np.uint64(99) + ids) ^ np.uint64(0x5DEECE66D)) & np.uint64((1 << 48) - 1)
 
     def step():
-        _lib.check(L.gz_fill_gaussians_host(0, 0, 0, n_streams, N_PER, p_st_in, p_st_out, None, None, p_sp, p_hs,
-                                            p_out, None, 1_000_000))
+        _lib.check(L.gz_fill_gaussians_host(1, 0, slot, n_streams, N_PER, p_st_in, p_st_out, None, None, None, None,
+                                            p_out, p_ck, 1_000_000))
         st_in[:] = st_out   # the streams continue (host-side hand-off, like the reference's write-back)
 
     for _ in range(warmup):
@@ -283,58 +322,119 @@ def e2e_host(first_id, n_streams, steps, warmup):
     dt = (time.perf_counter() - t0) / steps
     for p in pin:
         L.gz_host_free(p)
-    return {"s_per_step": dt, "h2d": n_streams * 8, "d2h": n_out * 8 + n_streams * 8 + n_streams * 9}
+    return {"s_per_step": dt, "h2d": n_streams * 8, "d2h": n_out * 8 + 2 * n_streams * 8}
 
 
-def cpu_reference(n_streams, steps, warmup, first_id=0):
-    """The reference algorithm on the host cores (oracle port, OpenMP)."""
+# ---------------------------------------------------------------- CPU baselines
+
+def cpu_port(n_streams, steps, warmup, first_id=0):
+    """The reference algorithm on the host cores: the oracle port (OpenMP over streams)."""
     import numpy as np
 
     from oracle import gz_oracle as O
 
     O.lib()
     threads = os.cpu_count() or 1
-    st = np.array([O.lcg_state(7 + i) for i in range(first_id, first_id + n_streams)], dtype=np.uint64)
+    st = O.config_states_range("c4", first_id, n_streams)
     for _ in range(warmup):
-        out, st, *_ = O.fill_gaussians("polar", "lcg48", st, N_PER, nthreads=threads)
+        dig, st, _, _, ps, status = O.fill_digest("ziggurat", "lcg48", st, N_PER, psum=True, nthreads=threads)
     ts = []
     for _ in range(steps):
         t0 = time.perf_counter()
-        out, st, sp, hs, status = O.fill_gaussians("polar", "lcg48", st, N_PER, nthreads=threads)
+        dig, st, _, _, ps, status = O.fill_digest("ziggurat", "lcg48", st, N_PER, psum=True, nthreads=threads)
         ts.append(time.perf_counter() - t0)
         assert status == 0
     dt = statistics.median(ts)
+    del np
     return {"value": n_streams * N_PER / dt, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"{n_streams} streams x {N_PER} variates of config 2 (polar x Lcg48(7+id)) per step, "
+            "cpu_model": cpu_model(),
+            "sample": f"{n_streams} streams x {N_PER} variates of config 4 (ziggurat x Lcg48(99+gid), "
+                      f"per-stream xor checksum + power sums, the deviates folded instead of stored) per step, "
                       f"median of {steps} steps, OpenMP over streams on {threads} threads"}
 
 
+def _numba_worker(args):
+    first, count, n_per, cache = args
+    os.environ.setdefault("NUMBA_CACHE_DIR", cache)
+    sys.path.insert(0, os.path.join(ROOT, "baseline", "_ref"))
+    import numpy as np
+
+    import gausszig
+    from gausszig import engine
+
+    buf = np.empty(n_per)
+    smp = gausszig.make_sampler("ziggurat")
+    engine.fill_gaussians(smp, gausszig.make_source("lcg48", 99), buf)   # JIT compile outside the timing
+    t0 = time.perf_counter()
+    acc = 0
+    for gid in range(first, first + count):
+        src = gausszig.make_source("lcg48", 99 + gid)
+        engine.fill_gaussians(smp, src, buf)
+        acc ^= int(np.bitwise_xor.reduce(buf.view(np.uint64)))
+    return time.perf_counter() - t0, acc
+
+
+def reference_as_is(n_streams=NUMBA_SAMPLE_STREAMS):
+    """The reference's own numba engine.fill_gaussians per stream (baseline/_ref), fanned
+    out over P = cpu_count worker processes each owning a contiguous block of streams
+    (the reference itself is single-threaded).  None when baseline/_ref is absent."""
+    if not os.path.isdir(os.path.join(ROOT, "baseline", "_ref", "gausszig")):
+        return None
+    import multiprocessing as mp
+
+    P = os.cpu_count() or 1
+    per = (n_streams + P - 1) // P
+    jobs = [(k * per, min(per, n_streams - k * per), N_PER, os.path.join("/tmp", "gz_numba_cache"))
+            for k in range(P) if k * per < n_streams]
+    try:
+        with mp.get_context("spawn").Pool(len(jobs)) as pool:
+            t0 = time.perf_counter()
+            res = pool.map(_numba_worker, jobs)
+            wall = time.perf_counter() - t0
+    except Exception as e:  # noqa: BLE001 -- report, do not fail the bench
+        return {"unavailable": f"{type(e).__name__}: {e}"}
+    slowest = max(r[0] for r in res)
+    return {"value": n_streams * N_PER / slowest, "unit": UNIT, "processes": len(jobs), "cpu_model": cpu_model(),
+            "kind": "reference (numba engine.fill_gaussians per stream, baseline/_ref)",
+            "sample": f"{n_streams} streams x {N_PER} variates of config 4, one engine.fill_gaussians call per "
+                      f"stream, contiguous stream blocks over {len(jobs)} processes; time = the slowest worker's "
+                      f"timed loop after its JIT warm-up (pool wall {wall:.2f} s incl. start-up and compile)"}
+
+
 def run_reference(args):
-    world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return 0
-    cb = cpu_reference(REF_SAMPLE_STREAMS, max(1, args.steps), max(1, min(args.warmup, 1)))
+    cb = cpu_port(REF_SAMPLE_STREAMS, max(1, args.steps), max(1, min(args.warmup, 1)))
     line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded streams)",
-            "config": {"workload": "config 2: polar x LCG48, 2^20 streams x 256 per GPU", "streams": REF_SAMPLE_STREAMS,
-                       "n_per": N_PER, "sample": "bounded CPU sample (see cpu_baseline.sample)"},
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded PRNG streams)",
+            "config": {"workload": WORKLOAD, "streams": REF_SAMPLE_STREAMS, "n_per": N_PER,
+                       "sample": "bounded CPU sample of the config-4 shard of rank 0 (see cpu_baseline.sample)"},
             "cpu_baseline": cb, "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
                                         "d2h_bytes_per_step": 0}, "world_size": world}
+    ra = reference_as_is()
+    if ra is not None:
+        line["reference_as_is"] = ra
     print(json.dumps(line), flush=True)
     return 0
 
 
+# ---------------------------------------------------------------- main
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-extra", action="store_true", help="skip the other four configs")
-    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baselines")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer end-to-end leg")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args)
     if args.impl == "reference":
         return run_reference(args)
     args.warmup = max(3, args.warmup)
@@ -344,83 +444,96 @@ def main():
     world, rank, local = dist_setup(args.gpus)
     hbm_peak, peak_kind = peaks()
 
-    # ---- headline: config 2 on every rank (weak scaling) ----
+    # ---- headline: config 4 on every rank (weak scaling), fused witnesses ----
     first = rank * STREAMS_PER_GPU
     with ClockSampler(local) as clk:
         time.sleep(0.3)   # let nvidia-smi start sampling before the timed region
-        r = time_fill("c2", first, STREAMS_PER_GPU, args.steps, args.warmup, world)
+        r = time_fill(HEAD, first, STREAMS_PER_GPU, args.steps, args.warmup, world, checks=True)
     ms = allmax(r["ms_per_step"], world)
     value = world * r["variates_per_step"] / (ms / 1e3)
     clocks = clk.summary()
     kernel_bytes = r["variates_per_step"] * 8
     achieved = kernel_bytes / (r["ms_per_step"] / 1e3) / 1e9
 
+    # the step's witnesses: global moments (Pebay/Chan merge in rank order) and xor
+    from paper_2405_19493_b200 import streams
+
+    cen = streams.central_from_psum(r["psum"], N_PER)
+    xr = streams.xor_fold(r["checksum"])
+    if world > 1:
+        from paper_2405_19493_b200 import dist as gzdist
+
+        merged = gzdist.gather_moments(cen)
+        xr = gzdist.gather_xor(xr)
+    else:
+        merged = tuple(cen.cpu().tolist())
+    m = streams.summarize(*merged)
+    witness = {"moments_last_step": {"n": m.n, "mean": m.mean, "variance": m.variance, "skewness": m.skewness,
+                                     "excess_kurtosis": m.excess_kurtosis},
+               "xor_all_streams_last_step": "%016x" % (xr & ((1 << 64) - 1))}
+    del r["checksum"], r["psum"]
+    torch.cuda.empty_cache()
+
     # ---- e2e through the host-buffer C-ABI call ----
-    e = e2e_host(first, STREAMS_PER_GPU, max(3, min(10, args.steps // 10)), 1)
-    e_s = allmax(e["s_per_step"] * 1e3, world) / 1e3
-    e2e = {"value": world * STREAMS_PER_GPU * N_PER / e_s, "unit": UNIT, "h2d_bytes_per_step": e["h2d"],
-           "d2h_bytes_per_step": e["d2h"], "s_per_step": e_s}
+    e2e = None
+    if not args.no_e2e:
+        e = e2e_host(first, STREAMS_PER_GPU, max(2, min(5, args.steps // 4)), 1)
+        e_s = allmax(e["s_per_step"] * 1e3, world) / 1e3
+        e2e = {"value": world * STREAMS_PER_GPU * N_PER / e_s, "unit": UNIT, "h2d_bytes_per_step": e["h2d"],
+               "d2h_bytes_per_step": e["d2h"], "s_per_step": e_s,
+               "path": "gz_fill_gaussians_host (pinned host buffers: states in; deviates, states, checksums out)"}
 
     # ---- the other configs (device time) ----
     extra = {}
     launches = r["launches"]
     if not args.no_extra:
-        c1 = time_fill("c1", 0, 1024, max(100, args.steps), args.warmup, world)
+        c1 = time_fill("c1", rank * 1024, 1024, max(100, args.steps), args.warmup, world)
         extra["c1"] = {"value": world * c1["variates_per_step"] / (allmax(c1["ms_per_step"], world) / 1e3),
-                       "ms_per_step": c1["ms_per_step"], "shape": "1024 x 4096 per GPU"}
+                       "ms_per_step": c1["ms_per_step"], "shape": "1024 x 4096 per GPU (rank r: stream ids r*1024..)"}
+        c2 = time_fill("c2", rank * (1 << 20), 1 << 20, max(5, args.steps // 2), args.warmup, world)
+        extra["c2"] = {"value": world * c2["variates_per_step"] / (allmax(c2["ms_per_step"], world) / 1e3),
+                       "ms_per_step": c2["ms_per_step"], "shape": "2^20 x 256 per GPU (polar x LCG48)"}
         n3 = (1 << 20) // world
-        c3 = time_fill("c3", rank * n3, n3, max(5, args.steps // 10), args.warmup, world)
+        c3 = time_fill("c3", rank * n3, n3, max(5, args.steps // 2), args.warmup, world)
         extra["c3"] = {"value": world * c3["variates_per_step"] / (allmax(c3["ms_per_step"], world) / 1e3),
                        "ms_per_step": c3["ms_per_step"], "shape": f"2^20 x 1024 box-wide, {n3} streams per GPU"}
-        c4 = time_fill("c4", rank * (1 << 22), 1 << 22, max(5, args.steps // 10), args.warmup, world, checks=True)
-        extra["c4"] = {"value": world * c4["variates_per_step"] / (allmax(c4["ms_per_step"], world) / 1e3),
-                       "ms_per_step": c4["ms_per_step"], "shape": "2^22 x 256 per GPU, fused checksum + moments"}
-        from paper_2405_19493_b200 import streams
-
-        cen = streams.central_from_psum(c4["psum"], 256)
-        xr = streams.xor_fold(c4["checksum"])
-        if world > 1:
-            from paper_2405_19493_b200 import dist as gzdist
-
-            merged = gzdist.gather_moments(cen)
-            xr = gzdist.gather_xor(xr)
-        else:
-            merged = tuple(cen.cpu().tolist())
-        m = streams.summarize(*merged)
-        extra["c4"]["moments"] = {"n": m.n, "mean": m.mean, "variance": m.variance, "excess_kurtosis": m.excess_kurtosis}
-        extra["c4"]["xor_all_streams"] = "%016x" % (xr & ((1 << 64) - 1))
-        del c4
         n5 = 65536 // world
-        c5 = time_mutate(rank * n5, n5, 10, max(3, args.steps // 20), args.warmup, world)
+        c5 = time_mutate(rank * n5, n5, 10, max(3, args.steps // 4), args.warmup, world)
         extra["c5"] = {"value": world * c5["variates_per_step"] / (allmax(c5["ms_per_step"], world) / 1e3),
                        "ms_per_step": c5["ms_per_step"],
                        "shape": f"65536 x 1024 genes box-wide ({n5} per GPU), 10 generations per step"}
         torch.cuda.empty_cache()
 
-    # ---- CPU baseline (rank 0, N = 1 only) ----
-    cpu = None
+    # ---- CPU baselines (rank 0, N = 1 only) ----
+    cpu = ref_numba = None
     if world == 1 and not args.no_cpu:
-        cpu = cpu_reference(REF_SAMPLE_STREAMS, 3, 1)
+        cpu = cpu_port(REF_SAMPLE_STREAMS, 3, 1)
+        ref_numba = reference_as_is()
 
     barrier(world)
     if rank == 0:
-        tr = traffic_record("c2")
+        tr = traffic_record(HEAD)
+        cb = compute_bounds(r["variates_per_step"] / (r["ms_per_step"] / 1e3), hbm_peak, clocks)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded PRNG streams)",
-            "config": {"workload": "config 2: polar x LCG48, 2^20 streams x 256 variates per GPU per step",
-                       "streams_per_gpu": STREAMS_PER_GPU, "n_per": N_PER, "seed": "Lcg48(7 + stream id)",
-                       "l2": "output 2 GiB per step > 126 MB L2 (no flush needed)", "parallelism": f"streams/{world}"},
+            "config": {"workload": WORKLOAD, "streams_per_gpu": STREAMS_PER_GPU, "n_per": N_PER,
+                       "seed": "Lcg48(99 + gid), GPU g owns gids [g*2^22, (g+1)*2^22)",
+                       "l2": "output 8 GiB per GPU per step > 126 MB L2 (no flush needed)",
+                       "parallelism": f"streams sharded over {world} GPU(s), no collective on the generation path"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                         "frac": achieved / hbm_peak, "traffic": tr, "peak_kind": peak_kind,
+                         "frac": achieved / hbm_peak, "traffic": None if tr is None else tr["bytes_per_launch"],
+                         "peak_kind": peak_kind, "kernel": "k_zig_tma (one launch per step)",
                          "algorithmic_bytes_per_launch": kernel_bytes,
-                         "compute_bounds": compute_bounds(r["variates_per_step"] / (r["ms_per_step"] / 1e3),
-                                                          hbm_peak, clocks)},
-            "e2e": e2e, "gpu_launches": launches, "clocks": clocks, "configs": extra,
+                         "traffic_source": None if tr is None else tr.get("source"),
+                         "compute_bounds": cb},
+            "e2e": e2e, "gpu_launches": launches, "clocks": clocks, "witness": witness, "configs": extra,
         }
         if cpu is not None:
             line["cpu_baseline"] = cpu
+        if ref_numba is not None:
+            line["reference_as_is"] = ref_numba
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist

@@ -29,7 +29,7 @@
  * accept/reject decisions and the order of the deviates are exactly the
  * reference's.
  *
- * Output by TMA.  The ring of a warp is TMA_NT tiles of 32 rows x 16 deviates
+ * Output by TMA.  The ring of a warp is NT tiles of 32 rows x 16 deviates
  * (4 KiB, the SWIZZLE_128B layout a TMA tensor box expects: the 16-byte chunk c
  * of row r sits at chunk c ^ (r & 7)).  When every lane of the warp has
  * produced 32 more deviates, one lane issues two tensor stores
@@ -40,8 +40,6 @@
  */
 #pragma once
 
-constexpr int TMA_K = 8;               /* attempts per lane per round */
-constexpr int TMA_NT = 4;              /* ring tiles per warp (power of two) */
 constexpr int TMA_TILE_BYTES = 32 * 128;
 constexpr int TMA_REP = 8;             /* replicas of the layer rows */
 constexpr uint64_t GZ_LCG_AINV = 0xDFE05BCB1365ULL;   /* 0x5DEECE66D^-1 mod 2^48 */
@@ -107,6 +105,16 @@ __device__ __forceinline__ void tma_split(uint64_t u, uint32_t& i, uint64_t& m, 
     }
 }
 
+/* one LCG48 step on 32-bit halves, (h:l) <- A*(h:l) + C mod 2^64 (only bits 0..47
+   matter): IMAD.WIDE.U32 of the low words with the increment, two IMADs for the
+   cross terms (A = 0x5_DEECE66D) */
+__device__ __forceinline__ void lcg_step32(uint32_t l, uint32_t h, uint32_t& ol, uint32_t& oh, uint64_t inc)
+{
+    const uint64_t p = (uint64_t)l * 0xDEECE66Du + inc;
+    ol = (uint32_t)p;
+    oh = (uint32_t)(p >> 32) + h * 0xDEECE66Du + l * 5u;
+}
+
 /* the draw cursor of one round.  LCG48: 32-bit halves of the unmasked state (bits
    above 47 are don't-care: they only reach bits >= 48 of later products); one
    u64 = two steps t1 = A*t + C, t2 = A*t1 + C, each one IMAD.WIDE.U32 and two
@@ -117,15 +125,16 @@ struct TmaCursor {
     uint32_t lo, hi;
     __device__ __forceinline__ explicit TmaCursor(uint64_t s) : lo((uint32_t)s), hi((uint32_t)(s >> 32)) {}
     __device__ __forceinline__ uint64_t state() const { return ((uint64_t)hi << 32) | lo; }
-    __device__ __forceinline__ void draw(uint64_t gam, uint32_t& uhi, uint32_t& ulo)
+    __device__ __forceinline__ void draw(uint64_t gam, uint64_t inc2, uint32_t& uhi, uint32_t& ulo)
     {
         if constexpr (SRC == 0) {
-            const uint64_t p1 = (uint64_t)lo * 0xDEECE66Du + 0xBu;
-            const uint32_t t1l = (uint32_t)p1;
-            const uint32_t t1h = (uint32_t)(p1 >> 32) + hi * 0xDEECE66Du + lo * 5u;
-            const uint64_t p2 = (uint64_t)t1l * 0xDEECE66Du + 0xBu;
-            const uint32_t t2l = (uint32_t)p2;
-            const uint32_t t2h = (uint32_t)(p2 >> 32) + t1h * 0xDEECE66Du + t1l * 5u;
+            uint32_t t1l, t1h, t2l, t2h;
+            lcg_step32(lo, hi, t1l, t1h, gam);   /* gam carries the increment 0xB for the LCG */
+            /* the second state straight from the first (A^2, A*C + C): the two steps
+               do not wait for each other */
+            const uint64_t p2 = (uint64_t)lo * 0xB4600A69u + inc2;
+            t2l = (uint32_t)p2;
+            t2h = (uint32_t)(p2 >> 32) + hi * 0xB4600A69u + lo * 0xBB20u;
             uhi = __funnelshift_r(t1l, t1h, 16);
             ulo = __funnelshift_r(t2l, t2h, 16);
             lo = t2l;
@@ -160,11 +169,23 @@ __device__ __forceinline__ void tma_split32(uint32_t uhi, uint32_t ulo, uint32_t
     }
 }
 
-/* ring slot of deviate w of this lane's row: tile (w / 16) mod TMA_NT, 16-byte
+/* ring slot of deviate w of this lane's row: tile (w / 16) mod NT, 16-byte
    chunk ((w mod 16) / 2) ^ (row mod 8) (SWIZZLE_128B), 8-byte half w mod 2 */
-__device__ __forceinline__ uint32_t tma_slot(uint32_t my_row, uint32_t lx, int w)
+/* Ring position counter.  Deviate w of a lane's row lives in ring tile
+   (w / 16) mod NT, 16-byte chunk ((w mod 16) / 2) ^ (row mod 8) (SWIZZLE_128B) and
+   8-byte half w mod 2.  The lane keeps
+       C(w) = (w / 16) << 12 | 0xF80 | (w mod 16) << 3
+   whose bits 7..11 are always ones, so C + 8 carries from the column bits straight
+   into the tile bits: advancing is one add and one OR, and the slot address is one
+   LOP3 ((C & tile|column mask) ^ row swizzle) plus the row base.  C is monotone in
+   w, so limits and the warp minimum compare C directly. */
+__device__ __forceinline__ uint32_t tma_cenc(int w) { return ((uint32_t)(w >> 4) << 12) | 0xF80u | ((uint32_t)(w & 15) << 3); }
+__device__ __forceinline__ int tma_cdec(uint32_t c) { return (int)(((c >> 12) << 4) | ((c >> 3) & 15u)); }
+__device__ __forceinline__ uint32_t tma_cinc(uint32_t c) { return (c + 8u) | 0xF80u; }
+template <int NT>
+__device__ __forceinline__ uint32_t tma_caddr(uint32_t my_row, uint32_t lx, uint32_t c)
 {
-    return my_row + (((uint32_t)w << 8) & ((TMA_NT - 1) << 12)) + ((((uint32_t)w << 3) & 0x78u) ^ lx);
+    return my_row + ((c & (((NT - 1u) << 12) | 0x78u)) ^ lx);
 }
 
 /* per-row witnesses, in deviate order: xor of the bit patterns (bench.py:174-175)
@@ -180,7 +201,7 @@ __device__ __forceinline__ void tma_fold(uint64_t zb, uint64_t& ck, double& a1, 
     a4 = __fma_rn(z2, z2, a4);
 }
 
-template <int SRC, bool MOD, bool STATS, int NW>
+template <int SRC, bool MOD, bool STATS, int NW, int NT, int FL, int TMA_K>
 __global__ void __launch_bounds__(NW * 32, 1) k_zig_tma(const __grid_constant__ LaneParams p,
                                                         const __grid_constant__ CUtensorMap tm)
 {
@@ -189,59 +210,109 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_tma(const __grid_constant__ 
     const uint32_t raw_sh = sh_addr(smem_raw);
     const uint32_t base_sh = (raw_sh + 1023u) & ~1023u;            /* SWIZZLE_128B tiles: 1 KiB aligned */
     unsigned char* base = smem_raw + (base_sh - raw_sh);
-    const uint32_t kw_sh = base_sh + NW * TMA_NT * TMA_TILE_BYTES;
-    ulonglong2* s_kw = reinterpret_cast<ulonglong2*>(base + NW * TMA_NT * TMA_TILE_BYTES);
-    float2* s_yf = reinterpret_cast<float2*>(base + NW * TMA_NT * TMA_TILE_BYTES + NL * 16 * TMA_REP);
+    constexpr uint32_t RING = NW * NT * TMA_TILE_BYTES;
+    const uint32_t kw_sh = base_sh + RING;
+    ulonglong2* s_kw = reinterpret_cast<ulonglong2*>(base + RING);
+    float2* s_yf = reinterpret_cast<float2*>(base + RING + NL * 16 * TMA_REP);
+    ulonglong2* s_jump = reinterpret_cast<ulonglong2*>(base + RING + NL * 16 * TMA_REP + NL * 8);
     for (int j = threadIdx.x; j < NL * TMA_REP; j += blockDim.x) s_kw[j] = p.kw[j / TMA_REP];
     for (int j = threadIdx.x; j < NL; j += blockDim.x) s_yf[j] = p.yf[j];
+    /* LCG: (A, C) of 2n steps, n <= TMA_K (the state after n draws from a round's start) */
+    if (SRC == 0 && threadIdx.x <= TMA_K) s_jump[threadIdx.x] = make_ulonglong2(c_lcgA[2 * threadIdx.x], c_lcgC[2 * threadIdx.x]);
     __syncthreads();
 
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
-    const uint32_t wring = base_sh + wib * TMA_NT * TMA_TILE_BYTES;
+    const uint32_t wring = base_sh + wib * NT * TMA_TILE_BYTES;
     const uint32_t my_row = wring + lane * 128;
     const uint32_t lx = (uint32_t)(lane & 7) << 4;                  /* the row's swizzle */
     const uint32_t my_kw = kw_sh + lx;                              /* replica lane & 7 */
     const uint32_t yf_sh = sh_addr(s_yf);
-    const int total = p.n_per;
+    const uint32_t jump_sh = sh_addr(s_jump);
+    /* LCG: the increments of one and two steps as opaque register pairs (an immediate
+       addend would split every IMAD.WIDE.U32 into a multiply and a 64-bit add) */
+    const uint64_t lcg_inc = SRC == 0 ? ld_keep(&c_lcgC[1]) : 0;
+    const uint64_t lcg_inc2 = SRC == 0 ? ld_keep(&c_lcgC[2]) : 0;
+    const int n_per = p.n_per;
     const uint32_t guard32 = p.guard > 0xffffffffll ? 0xffffffffu : (uint32_t)p.guard;
     const int64_t n_streams = p.n_streams;
     const int64_t n_groups = (n_streams + 31) >> 5;
     const int64_t gstride = (int64_t)gridDim.x * NW;
-    constexpr int SLACK = (TMA_NT - 2) * 16;                       /* columns writable past the flushed ones */
+    constexpr int FB = FL * 16;                                    /* columns per flush */
+    constexpr int SLACK = (NT - FL) * 16;                          /* columns writable past the flushed ones */
+    static_assert((NT & (NT - 1)) == 0 && FL <= NT / 2, "ring: power-of-two tiles, at most half in flight");
 
-    for (int64_t grp = (int64_t)blockIdx.x * NW + wib; grp < n_groups; grp += gstride) {
-        const int64_t row0 = grp * 32;
-        const int64_t sid = row0 + lane;
-        const bool valid = sid < n_streams;
-        uint64_t S = 0, gam = 0;
-        if (valid) {
-            if constexpr (SRC == 0) {
-                S = p.state_in[sid];
-            } else {
-                S = p.state_in[2 * sid];
-                gam = p.state_in[2 * sid + 1];
-            }
-        }
-        int w = valid ? 0 : total;     /* deviates produced */
-        int flushed = 0;               /* columns handed to TMA (warp-uniform) */
-        int lim = min(total, TMA_NT * 16);   /* nothing in flight yet: the whole ring */
-        uint32_t rej = 0;
-        int w_rej = -1;
-        bool failed = false;
+    /* The warp's rows (32 streams each: groups g0, g0 + gstride, ...) are one
+       continuous sequence of ring columns, rowlen = n_per rounded up to a tile per
+       row, so a lane that finishes a row starts its next row at once instead of
+       waiting at the row end for the slowest lane of the warp. */
+    const int64_t g0 = (int64_t)blockIdx.x * NW + wib;
+    if (g0 < n_groups) {
+        const int rowlen = (n_per + 15) & ~15;
+        const int ng = (int)((n_groups - g0 + gstride - 1) / gstride);
+        const int wtot = ng * rowlen;                 /* ring columns of this warp */
+        const uint32_t c_end = tma_cenc(wtot);
+
+        int k = -1;                   /* this lane's current row */
+        int64_t sid = 0;
+        bool valid = false, failed = false;
+        uint64_t S = 0, gam = lcg_inc;
+        uint32_t C = tma_cenc(0), c_rowend = tma_cenc(0);
+        uint32_t rej = 0, c_rej = 0xffffffffu;
+        int flushed = 0;                                          /* columns handed to TMA (warp-uniform) */
+        uint32_t c_lim = tma_cenc(min(wtot, NT * 16));            /* nothing in flight yet: the whole ring */
+        uint32_t c_limr = 0;                                      /* min(c_lim, c_rowend) */
         uint64_t ck = 0;
         double a1 = 0.0, a2 = 0.0, a3 = 0.0, a4 = 0.0;
+
+        /* row transitions (divergent, once per row and lane): store the finished
+           row's state, load the next row's */
+        auto next_rows = [&]() {
+            while (C >= c_rowend && k < ng) {
+                if (valid && !failed) {
+                    if constexpr (SRC == 0) {
+                        p.state_out[sid] = S & GZ_MASK48;
+                    } else {
+                        p.state_out[2 * sid] = S;
+                        p.state_out[2 * sid + 1] = gam;
+                    }
+                }
+                ++k;
+                failed = false;
+                if (k < ng) {
+                    sid = (g0 + k * gstride) * 32 + lane;
+                    valid = sid < n_streams;
+                    if (valid) {
+                        if constexpr (SRC == 0) {
+                            S = p.state_in[sid];
+                        } else {
+                            S = p.state_in[2 * sid];
+                            gam = p.state_in[2 * sid + 1];
+                        }
+                        C = tma_cenc(k * rowlen);
+                        c_rowend = tma_cenc(k * rowlen + n_per);
+                    } else {
+                        C = c_rowend = tma_cenc((k + 1) * rowlen);   /* no stream: skip the row */
+                    }
+                } else {
+                    valid = false;
+                    C = c_end;
+                }
+            }
+            c_limr = min(c_lim, c_rowend);
+        };
+        next_rows();
 
         while (true) {
             /* ---- one round: TMA_K attempts per lane, no branches ---- */
             bool frozen = false;
+            const uint32_t C0 = C;
             TmaCursor<SRC> t(S);
 #pragma unroll
-            for (int k = 0; k < TMA_K; ++k) {
-                const bool live = !frozen && w < lim;
+            for (int kk2 = 0; kk2 < TMA_K; ++kk2) {
+                const bool live = !frozen && C < c_limr;
                 uint32_t uhi, ulo;
-                t.draw(gam, uhi, ulo);
-                if (live) S = t.state();
+                t.draw(gam, lcg_inc2, uhi, ulo);
                 uint32_t ioff, mhi, mlo, sgn;
                 tma_split32<MOD>(uhi, ulo, ioff, mhi, mlo, sgn);
                 uint64_t kk, wb;
@@ -251,13 +322,24 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_tma(const __grid_constant__ 
                 const bool ok = m < kk;
                 const bool commit = live && ok;
                 frozen = frozen || (live && !ok);
-                /* the commit is predicated, not branched: a skipped attempt folds +0.0 into
-                   the witnesses, which leaves every sum (never -0.0) and the xor unchanged */
-                const uint64_t zb = commit ? ((uint64_t)__double_as_longlong(x) ^ ((uint64_t)sgn << 32)) : 0ull;
-                const uint32_t a = tma_slot(my_row, lx, w);
-                if (commit) asm volatile("st.shared.u64 [%0], %1;" ::"r"(a), "l"(zb) : "memory");
-                if constexpr (STATS) tma_fold(zb, ck, a1, a2, a3, a4);
-                w += commit ? 1 : 0;
+                const uint64_t zb = (uint64_t)__double_as_longlong(x) ^ ((uint64_t)sgn << 32);
+                const uint32_t a = tma_caddr<NT>(my_row, lx, C);
+                if (commit) {
+                    asm volatile("st.shared.u64 [%0], %1;" ::"r"(a), "l"(zb) : "memory");
+                    C = tma_cinc(C);
+                }
+            }
+            /* the live attempts are a prefix of the round: the committed ones plus a
+               frozen one; the state after them by jump-ahead from the round's start */
+            {
+                const uint32_t n_live = (uint32_t)(tma_cdec(C) - tma_cdec(C0)) + (frozen ? 1u : 0u);
+                if constexpr (SRC == 0) {
+                    uint64_t ja, jc;
+                    lds_u64x2_v(jump_sh + 16 * n_live, ja, jc);
+                    S = S * ja + jc;
+                } else {
+                    S += (uint64_t)n_live * gam;
+                }
             }
             /* ---- the frozen lanes' slow attempts, resolved together ---- */
             if (__any_sync(GZ_FULL, frozen)) {
@@ -275,11 +357,12 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_tma(const __grid_constant__ 
                         const uint64_t u2 = tma_draw<SRC>(S, gam);
                         ok = wedge_accept_f(u2, x, p.yd + i, lds_f32x2(yf_sh + 8 * i));
                         if (!ok) {
-                            rej = (w == w_rej) ? rej + 1 : 1;   /* consecutive rejections */
-                            w_rej = w;
+                            rej = (C == c_rej) ? rej + 1 : 1;   /* consecutive rejections */
+                            c_rej = C;
                             if (rej >= guard32) {
                                 failed = true;
-                                w = total;
+                                gz_raise(GZ_ERR_GUARD, sid);
+                                C = c_rowend;
                             }
                         }
                     } else {
@@ -289,62 +372,79 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_tma(const __grid_constant__ 
                         ok = to.k >= 0;
                         if (!ok) {
                             failed = true;
-                            w = total;
+                            gz_raise(GZ_ERR_GUARD, sid);
+                            C = c_rowend;
                         }
                     }
                     if (ok) {
                         const uint64_t zb = (uint64_t)__double_as_longlong(x) ^ sgn;
-                        asm volatile("st.shared.u64 [%0], %1;" ::"r"(tma_slot(my_row, lx, w)), "l"(zb) : "memory");
-                        if constexpr (STATS) tma_fold(zb, ck, a1, a2, a3, a4);
-                        ++w;
+                        asm volatile("st.shared.u64 [%0], %1;" ::"r"(tma_caddr<NT>(my_row, lx, C)), "l"(zb) : "memory");
+                        C = tma_cinc(C);
                     }
                 }
             }
-            /* ---- hand complete 32-column blocks to TMA ---- */
-            const int minw = (int)__reduce_min_sync(GZ_FULL, (unsigned)w);
-            while (minw - flushed >= 32 || (minw >= total && flushed < total)) {
-                const int cnt = min(32, total - flushed);
+            next_rows();
+            /* ---- hand complete blocks of FB columns to TMA ---- */
+            const int minw = tma_cdec(__reduce_min_sync(GZ_FULL, C));
+            while (minw - flushed >= FB || (minw >= wtot && flushed < wtot)) {
+                const int cnt = min(FB, wtot - flushed);
+                if constexpr (STATS) {
+                    /* per-row witnesses, folded in deviate order from this lane's row of
+                       the tiles (stats.py:232-259 power sums, bench.py:174-175 xor) */
+#pragma unroll
+                    for (int j = 0; j < FL; ++j) {
+                        const int lc = flushed + 16 * j;
+                        if (16 * j < cnt) {
+                            const int kt = lc / rowlen;
+                            const int col = lc - kt * rowlen;
+                            const uint32_t trow = wring + ((lc >> 4) & (NT - 1)) * TMA_TILE_BYTES + lane * 128;
+#pragma unroll
+                            for (int c2 = 0; c2 < 8; ++c2) {
+                                uint64_t v0, v1;
+                                lds_u64x2_v(trow + (((uint32_t)c2 << 4) ^ lx), v0, v1);
+                                if (col + 2 * c2 < n_per) tma_fold(v0, ck, a1, a2, a3, a4);
+                                if (col + 2 * c2 + 1 < n_per) tma_fold(v1, ck, a1, a2, a3, a4);
+                            }
+                            if (col + 16 >= n_per) {
+                                /* the row's last tile: its witnesses are complete */
+                                const int64_t tsid = (g0 + (int64_t)kt * gstride) * 32 + lane;
+                                if (tsid < n_streams) {
+                                    if (p.checksum) p.checksum[tsid] = ck;
+                                    if (p.psum) {
+                                        p.psum[4 * tsid + 0] = a1;
+                                        p.psum[4 * tsid + 1] = a2;
+                                        p.psum[4 * tsid + 2] = a3;
+                                        p.psum[4 * tsid + 3] = a4;
+                                    }
+                                }
+                                ck = 0;
+                                a1 = a2 = a3 = a4 = 0.0;
+                            }
+                        }
+                    }
+                }
                 fence_async_smem();
                 __syncwarp();
                 if (lane == 0) {
-                    tma_wait_read_all();   /* the previous block (issued >= 32 columns ago) */
-                    const int tile = (flushed >> 4) & (TMA_NT - 1);
-                    tma_store_tile(&tm, wring + tile * TMA_TILE_BYTES, flushed, (int)row0);
-                    if (cnt > 16)
-                        tma_store_tile(&tm, wring + ((tile + 1) & (TMA_NT - 1)) * TMA_TILE_BYTES, flushed + 16,
-                                       (int)row0);
+                    tma_wait_read_all();   /* the previous block (issued >= FB columns ago) */
+#pragma unroll
+                    for (int j = 0; j < FL; ++j) {
+                        const int lc = flushed + 16 * j;
+                        if (16 * j < cnt) {
+                            const int kt = lc / rowlen;
+                            tma_store_tile(&tm, wring + ((lc >> 4) & (NT - 1)) * TMA_TILE_BYTES, lc - kt * rowlen,
+                                           (int)((g0 + (int64_t)kt * gstride) * 32));
+                        }
+                    }
                     tma_commit();
                 }
                 __syncwarp();
                 flushed += cnt;
-                lim = min(total, flushed + SLACK);   /* the tiles of the block just freed */
+                c_lim = tma_cenc(min(wtot, flushed + SLACK));   /* the tiles of the block just freed */
+                c_limr = min(c_lim, c_rowend);
             }
-            if (minw >= total) break;   /* every row complete and handed to TMA */
+            if (minw >= wtot) break;   /* every row complete and handed to TMA */
         }
-        if (valid) {
-            if (failed) {
-                gz_raise(GZ_ERR_GUARD, sid);
-            } else {
-                if constexpr (SRC == 0) {
-                    p.state_out[sid] = S & GZ_MASK48;
-                } else {
-                    p.state_out[2 * sid] = S;
-                    p.state_out[2 * sid + 1] = gam;
-                }
-                if constexpr (STATS) {
-                    if (p.checksum) p.checksum[sid] = ck;
-                    if (p.psum) {
-                        p.psum[4 * sid + 0] = a1;
-                        p.psum[4 * sid + 1] = a2;
-                        p.psum[4 * sid + 2] = a3;
-                        p.psum[4 * sid + 3] = a4;
-                    }
-                }
-            }
-        }
-        /* the ring is reused by the next group: its last blocks must have been read */
-        if (lane == 0) tma_wait_read_all();
-        __syncwarp();
+        if (lane == 0) tma_wait_all();
     }
-    if (lane == 0) tma_wait_all();
 }
