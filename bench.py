@@ -56,8 +56,10 @@ METRIC = "fp64 Gaussian variates/sec (ziggurat x LCG48, config 4, fused per-stre
 UNIT = "variates/s"
 WORKLOAD = "config 4: original ziggurat (128 layers) x LCG48, 2^22 streams x 256 variates per GPU per step, " \
            "fused per-stream xor checksums + power sums, global moments merged over ranks"
-REF_SAMPLE_STREAMS = 1 << 20     # CPU sample per step: 2^20 streams x 256 = 2^28 variates of config 4
-NUMBA_SAMPLE_STREAMS = 1 << 14   # reference-as-is sample: 2^14 streams x 256, one engine call per stream
+# CPU sample per step: 2^20 streams x 256 = 2^28 variates of config 4 (env overrides: tests only)
+REF_SAMPLE_STREAMS = int(os.environ.get("GZ_BENCH_REF_STREAMS", 1 << 20))
+# reference-as-is sample: 2^14 streams x 256, one engine call per stream
+NUMBA_SAMPLE_STREAMS = int(os.environ.get("GZ_BENCH_NUMBA_STREAMS", 1 << 14))
 
 
 def peaks():

@@ -190,6 +190,16 @@ __device__ __forceinline__ uint32_t tma_caddr(uint32_t my_row, uint32_t lx, uint
 
 /* per-row witnesses, in deviate order: xor of the bit patterns (bench.py:174-175)
    and the power sums the moments are merged from (stats.py:232-259) */
+__device__ __forceinline__ void tma_fold_fp(uint64_t zb, double& a1, double& a2, double& a3, double& a4)
+{
+    const double z = __longlong_as_double((long long)zb);
+    const double z2 = __dmul_rn(z, z);
+    a1 = __dadd_rn(a1, z);
+    a2 = __dadd_rn(a2, z2);
+    a3 = __fma_rn(z2, z, a3);
+    a4 = __fma_rn(z2, z2, a4);
+}
+
 __device__ __forceinline__ void tma_fold(uint64_t zb, uint64_t& ck, double& a1, double& a2, double& a3, double& a4)
 {
     const double z = __longlong_as_double((long long)zb);
@@ -260,6 +270,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_tma(const __grid_constant__ 
         uint32_t C = tma_cenc(0), c_rowend = tma_cenc(0);
         uint32_t rej = 0, c_rej = 0xffffffffu;
         int flushed = 0;                                          /* columns handed to TMA (warp-uniform) */
+        int fk = 0, fcol = 0;                                     /* the flush position: row, column */
         uint32_t c_lim = tma_cenc(min(wtot, NT * 16));            /* nothing in flight yet: the whole ring */
         uint32_t c_limr = 0;                                      /* min(c_lim, c_rowend) */
         uint64_t ck = 0;
@@ -393,21 +404,30 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_tma(const __grid_constant__ 
                        the tiles (stats.py:232-259 power sums, bench.py:174-175 xor) */
 #pragma unroll
                     for (int j = 0; j < FL; ++j) {
-                        const int lc = flushed + 16 * j;
                         if (16 * j < cnt) {
-                            const int kt = lc / rowlen;
-                            const int col = lc - kt * rowlen;
-                            const uint32_t trow = wring + ((lc >> 4) & (NT - 1)) * TMA_TILE_BYTES + lane * 128;
+                            const int col = fcol + 16 * j;   /* FL > 1 needs rowlen % (16 FL) == 0 */
+                            const uint32_t trow =
+                                wring + (((flushed >> 4) + j) & (NT - 1)) * TMA_TILE_BYTES + lane * 128;
+                            if (col + 16 <= n_per) {
 #pragma unroll
-                            for (int c2 = 0; c2 < 8; ++c2) {
-                                uint64_t v0, v1;
-                                lds_u64x2_v(trow + (((uint32_t)c2 << 4) ^ lx), v0, v1);
-                                if (col + 2 * c2 < n_per) tma_fold(v0, ck, a1, a2, a3, a4);
-                                if (col + 2 * c2 + 1 < n_per) tma_fold(v1, ck, a1, a2, a3, a4);
+                                for (int c2 = 0; c2 < 8; ++c2) {
+                                    uint64_t v0, v1;
+                                    lds_u64x2_v(trow + (((uint32_t)c2 << 4) ^ lx), v0, v1);
+                                    ck ^= v0 ^ v1;
+                                    tma_fold_fp(v0, a1, a2, a3, a4);
+                                    tma_fold_fp(v1, a1, a2, a3, a4);
+                                }
+                            } else {
+                                for (int c2 = 0; c2 < 8; ++c2) {
+                                    uint64_t v0, v1;
+                                    lds_u64x2_v(trow + (((uint32_t)c2 << 4) ^ lx), v0, v1);
+                                    if (col + 2 * c2 < n_per) tma_fold(v0, ck, a1, a2, a3, a4);
+                                    if (col + 2 * c2 + 1 < n_per) tma_fold(v1, ck, a1, a2, a3, a4);
+                                }
                             }
                             if (col + 16 >= n_per) {
                                 /* the row's last tile: its witnesses are complete */
-                                const int64_t tsid = (g0 + (int64_t)kt * gstride) * 32 + lane;
+                                const int64_t tsid = (g0 + (int64_t)fk * gstride) * 32 + lane;
                                 if (tsid < n_streams) {
                                     if (p.checksum) p.checksum[tsid] = ck;
                                     if (p.psum) {
@@ -429,17 +449,19 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_tma(const __grid_constant__ 
                     tma_wait_read_all();   /* the previous block (issued >= FB columns ago) */
 #pragma unroll
                     for (int j = 0; j < FL; ++j) {
-                        const int lc = flushed + 16 * j;
-                        if (16 * j < cnt) {
-                            const int kt = lc / rowlen;
-                            tma_store_tile(&tm, wring + ((lc >> 4) & (NT - 1)) * TMA_TILE_BYTES, lc - kt * rowlen,
-                                           (int)((g0 + (int64_t)kt * gstride) * 32));
-                        }
+                        if (16 * j < cnt)
+                            tma_store_tile(&tm, wring + (((flushed >> 4) + j) & (NT - 1)) * TMA_TILE_BYTES,
+                                           fcol + 16 * j, (int)((g0 + (int64_t)fk * gstride) * 32));
                     }
                     tma_commit();
                 }
                 __syncwarp();
                 flushed += cnt;
+                fcol += cnt;
+                if (fcol >= rowlen) {
+                    fcol = 0;
+                    ++fk;
+                }
                 c_lim = tma_cenc(min(wtot, flushed + SLACK));   /* the tiles of the block just freed */
                 c_limr = min(c_lim, c_rowend);
             }
