@@ -16,7 +16,10 @@
  * Compiled both for the device (nvcc, explicit __fma_rn/__dmul_rn/... so that
  * no contraction can change an operation) and for the host (gcc/g++ with
  * -ffp-contract=off, fma() from <math.h>), so the restatement is sweep-checked
- * against the real libm on the CPU without a GPU (tests/test_libm_restatement.py).
+ * against the real libm on the CPU without a GPU (tests/test_host_api.py, the
+ * host sweep; tests/test_gpu_parity.py test_device_libm_bit_exact_sweep on the device).
+ * Table and coefficient data: glibc (LGPL-2.1+; the optimized-routines exp/log,
+ * MIT/Apache-2.0 upstream) -- see NOTICE.
  */
 #pragma once
 #include <stdint.h>
