@@ -386,6 +386,7 @@ __global__ void __launch_bounds__(LANE_THREADS, EPI == EPI_MUTATE ? 2 : 3) k_zig
                         /* sign by bit flip: identical to the reference's negation */
                         const double z = __longlong_as_double((long long)((uint64_t)__double_as_longlong(x) ^ sgn));
                         const uint32_t slot = myring_sh + 8 * (w & (LRING - 1));
+                        GZ_CHECK(w < lim && w - flushed < LRING, w - flushed);
                         if constexpr (EPI == EPI_MUTATE) {
                             sts_f64(slot, __dadd_rn(lds_f64(slot), __dmul_rn(sig, z)));
                         } else {
@@ -398,6 +399,7 @@ __global__ void __launch_bounds__(LANE_THREADS, EPI == EPI_MUTATE ? 2 : 3) k_zig
             const int lag = (int)__reduce_min_sync(GZ_FULL, (unsigned)(w - flushed));
             const bool done = __all_sync(GZ_FULL, w >= total);
             const int cnt = lag >= LK ? LK : (done ? total - flushed : 0);
+            GZ_CHECK(cnt >= 0 && cnt <= LK && fcol >= 0, cnt);
             if (cnt > 0) {
                 __syncwarp();
                 if constexpr (STATS) {

@@ -161,7 +161,10 @@ struct LsegShared {
 };
 
 template <int SRC, int IBT, bool MOD>
-__global__ void __launch_bounds__(32 * LSEG_MAXP, SRC == 1 ? 3 : 2) k_zig_lseg(const __grid_constant__ LaneParams p, const LsegParams sp)
+#ifndef LSEG_MINB1
+#define LSEG_MINB1 3   /* blocks per SM the SplitMix64 form is compiled for */
+#endif
+__global__ void __launch_bounds__(32 * LSEG_MAXP, SRC == 1 ? LSEG_MINB1 : 2) k_zig_lseg(const __grid_constant__ LaneParams p, const LsegParams sp)
 {
     extern __shared__ __align__(16) unsigned char smem[];
     const int nl = IBT ? (1 << IBT) : p.n_layers;

@@ -335,6 +335,9 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_tma(const __grid_constant__ 
                 frozen = frozen || (live && !ok);
                 const uint64_t zb = (uint64_t)__double_as_longlong(x) ^ ((uint64_t)sgn << 32);
                 const uint32_t a = tma_caddr<NT>(my_row, lx, C);
+                GZ_CHECK(ioff < NL * 128u, ioff);
+                GZ_CHECK(!commit || (a >= wring && a < wring + NT * TMA_TILE_BYTES), a - wring);
+                GZ_CHECK(!commit || tma_cdec(C) < flushed + SLACK + FB, tma_cdec(C) - flushed);
                 if (commit) {
                     asm volatile("st.shared.u64 [%0], %1;" ::"r"(a), "l"(zb) : "memory");
                     C = tma_cinc(C);
@@ -344,6 +347,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_tma(const __grid_constant__ 
                frozen one; the state after them by jump-ahead from the round's start */
             {
                 const uint32_t n_live = (uint32_t)(tma_cdec(C) - tma_cdec(C0)) + (frozen ? 1u : 0u);
+                GZ_CHECK(n_live <= (uint32_t)TMA_K, n_live);
                 if constexpr (SRC == 0) {
                     uint64_t ja, jc;
                     lds_u64x2_v(jump_sh + 16 * n_live, ja, jc);
@@ -387,7 +391,9 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_tma(const __grid_constant__ 
                             C = c_rowend;
                         }
                     }
+                    GZ_CHECK(i < (uint32_t)NL, i);
                     if (ok) {
+                        GZ_CHECK(C < c_limr, tma_cdec(C));
                         const uint64_t zb = (uint64_t)__double_as_longlong(x) ^ sgn;
                         asm volatile("st.shared.u64 [%0], %1;" ::"r"(tma_caddr<NT>(my_row, lx, C)), "l"(zb) : "memory");
                         C = tma_cinc(C);
@@ -399,6 +405,8 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_tma(const __grid_constant__ 
             const int minw = tma_cdec(__reduce_min_sync(GZ_FULL, C));
             while (minw - flushed >= FB || (minw >= wtot && flushed < wtot)) {
                 const int cnt = min(FB, wtot - flushed);
+                GZ_CHECK(cnt > 0 && flushed + cnt <= minw && fk < ng && fcol < rowlen, fcol);
+                GZ_CHECK(fk * rowlen + fcol == flushed, flushed);
                 if constexpr (STATS) {
                     /* per-row witnesses, folded in deviate order from this lane's row of
                        the tiles (stats.py:232-259 power sums, bench.py:174-175 xor) */
