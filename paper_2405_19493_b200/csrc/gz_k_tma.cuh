@@ -250,7 +250,10 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_tma(const __grid_constant__ 
     const int64_t gstride = (int64_t)gridDim.x * NW;
     constexpr int FB = FL * 16;                                    /* columns per flush */
     constexpr int SLACK = (NT - FL) * 16;                          /* columns writable past the flushed ones */
-    static_assert((NT & (NT - 1)) == 0 && FL <= NT / 2, "ring: power-of-two tiles, at most half in flight");
+    static_assert(((NT & (NT - 1)) == 0 || NT == 3) && FL <= NT / 2, "ring: 3 or a power of two tiles, at most half in flight");
+    /* ring slot of a tile (a power-of-two ring: mask; three tiles: the lane tracks its
+       tile's byte offset tb, advanced when the column bits of C wrap) */
+    auto slot_of = [](int tile) { return (NT & (NT - 1)) == 0 ? (tile & (NT - 1)) : tile % NT; };
 
     /* The warp's rows (32 streams each: groups g0, g0 + gstride, ...) are one
        continuous sequence of ring columns, rowlen = n_per rounded up to a tile per
@@ -268,6 +271,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_tma(const __grid_constant__ 
         bool valid = false, failed = false;
         uint64_t S = 0, gam = lcg_inc;
         uint32_t C = tma_cenc(0), c_rowend = tma_cenc(0);
+        uint32_t tb = 0;              /* NT == 3: byte offset of C's ring tile */
         uint32_t rej = 0, c_rej = 0xffffffffu;
         int flushed = 0;                                          /* columns handed to TMA (warp-uniform) */
         int fk = 0, fcol = 0;                                     /* the flush position: row, column */
@@ -302,6 +306,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_tma(const __grid_constant__ 
                         }
                         C = tma_cenc(k * rowlen);
                         c_rowend = tma_cenc(k * rowlen + n_per);
+                        if constexpr (NT == 3) tb = (uint32_t)slot_of((k * rowlen) >> 4) * TMA_TILE_BYTES;
                     } else {
                         C = c_rowend = tma_cenc((k + 1) * rowlen);   /* no stream: skip the row */
                     }
@@ -334,13 +339,16 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_tma(const __grid_constant__ 
                 const bool commit = live && ok;
                 frozen = frozen || (live && !ok);
                 const uint64_t zb = (uint64_t)__double_as_longlong(x) ^ ((uint64_t)sgn << 32);
-                const uint32_t a = tma_caddr<NT>(my_row, lx, C);
+                const uint32_t a = NT == 3 ? my_row + tb + ((C & 0x78u) ^ lx) : tma_caddr<NT>(my_row, lx, C);
                 GZ_CHECK(ioff < NL * 128u, ioff);
                 GZ_CHECK(!commit || (a >= wring && a < wring + NT * TMA_TILE_BYTES), a - wring);
                 GZ_CHECK(!commit || tma_cdec(C) < flushed + SLACK + FB, tma_cdec(C) - flushed);
                 if (commit) {
                     asm volatile("st.shared.u64 [%0], %1;" ::"r"(a), "l"(zb) : "memory");
                     C = tma_cinc(C);
+                    if constexpr (NT == 3) {
+                        if ((C & 0x78u) == 0) tb = tb == 2u * TMA_TILE_BYTES ? 0u : tb + TMA_TILE_BYTES;
+                    }
                 }
             }
             /* the live attempts are a prefix of the round: the committed ones plus a
@@ -395,8 +403,12 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_tma(const __grid_constant__ 
                     if (ok) {
                         GZ_CHECK(C < c_limr, tma_cdec(C));
                         const uint64_t zb = (uint64_t)__double_as_longlong(x) ^ sgn;
-                        asm volatile("st.shared.u64 [%0], %1;" ::"r"(tma_caddr<NT>(my_row, lx, C)), "l"(zb) : "memory");
+                        const uint32_t a = NT == 3 ? my_row + tb + ((C & 0x78u) ^ lx) : tma_caddr<NT>(my_row, lx, C);
+                        asm volatile("st.shared.u64 [%0], %1;" ::"r"(a), "l"(zb) : "memory");
                         C = tma_cinc(C);
+                        if constexpr (NT == 3) {
+                            if ((C & 0x78u) == 0) tb = tb == 2u * TMA_TILE_BYTES ? 0u : tb + TMA_TILE_BYTES;
+                        }
                     }
                 }
             }
@@ -415,7 +427,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_tma(const __grid_constant__ 
                         if (16 * j < cnt) {
                             const int col = fcol + 16 * j;   /* FL > 1 needs rowlen % (16 FL) == 0 */
                             const uint32_t trow =
-                                wring + (((flushed >> 4) + j) & (NT - 1)) * TMA_TILE_BYTES + lane * 128;
+                                wring + slot_of((flushed >> 4) + j) * TMA_TILE_BYTES + lane * 128;
                             if (col + 16 <= n_per) {
 #pragma unroll
                                 for (int c2 = 0; c2 < 8; ++c2) {
@@ -458,7 +470,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_tma(const __grid_constant__ 
 #pragma unroll
                     for (int j = 0; j < FL; ++j) {
                         if (16 * j < cnt)
-                            tma_store_tile(&tm, wring + (((flushed >> 4) + j) & (NT - 1)) * TMA_TILE_BYTES,
+                            tma_store_tile(&tm, wring + slot_of((flushed >> 4) + j) * TMA_TILE_BYTES,
                                            fcol + 16 * j, (int)((g0 + (int64_t)fk * gstride) * 32));
                     }
                     tma_commit();
@@ -478,3 +490,4 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_tma(const __grid_constant__ 
         if (lane == 0) tma_wait_all();
     }
 }
+

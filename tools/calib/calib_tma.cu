@@ -95,6 +95,36 @@ __global__ void __launch_bounds__(NW * 32) k_store(const __grid_constant__ CUten
     if (MODE != 0 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+/* mode 4: every lane copies its own row segment (SEG doubles) with a 1D bulk copy
+   (cp.async.bulk, SASS UBLKCP) from a private padded ring row, no warp coupling */
+template <int SEG, int NW>
+__global__ void __launch_bounds__(NW * 32) k_lanebulk(int64_t n_rows, int n_per, double* out, uint64_t seed)
+{
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    constexpr int RS = 2 * SEG * 8 + 16;            /* ring row stride: two segments + 16 B pad */
+    unsigned char* row = smem_raw + ((size_t)wib * 32 + lane) * RS;
+    const uint32_t row_sh = (uint32_t)__cvta_generic_to_shared(row);
+    const int64_t n_groups = n_rows / 32;
+    for (int64_t grp = (int64_t)blockIdx.x * NW + wib; grp < n_groups; grp += (int64_t)gridDim.x * NW) {
+        const int64_t r = grp * 32 + lane;
+        uint64_t S = seed + r;
+        int half = 0;
+        for (int f = 0; f < n_per; f += SEG) {
+            asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");   /* this half's previous copy */
+            const uint32_t hb = row_sh + half * SEG * 8;
+#pragma unroll 4
+            for (int c = 0; c < SEG; ++c) sts64(hb + 8 * c, (double)(lcg2(S) >> 11));
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(out + r * n_per + f),
+                         "r"(hb), "n"(SEG * 8) : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            half ^= 1;
+        }
+    }
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 template <int REP>
 __global__ void __launch_bounds__(256) k_gather(const ulonglong2* tab, int iters, uint64_t* sink)
 {
@@ -152,10 +182,29 @@ int main()
     run(k_store<0, 8>, 8, 8 * 32 * 33 * 8 * 2 + 1024, "lanes STG.128 (128 B segments)");
     run(k_store<1, 8>, 8, 8 * 4 * 4096 + 1024, "TMA 16 cols/flush (128 B)");
     run(k_store<2, 8>, 8, 8 * 4 * 4096 + 1024, "TMA 32 cols/flush (256 B)");
-    run(k_store<3, 8>, 8, 8 * 8 * 4096 + 1024, "TMA 64 cols/flush (512 B)");
     run(k_store<1, 4>, 4, 4 * 4 * 4096 + 1024, "TMA 16 cols/flush, 4-warp blocks");
     run(k_store<2, 4>, 4, 4 * 4 * 4096 + 1024, "TMA 32 cols/flush, 4-warp blocks");
-    run(k_store<2, 16>, 16, 16 * 4 * 4096 + 1024, "TMA 32 cols/flush, 16-warp blocks");
+    auto runl = [&](auto kern, int nw, size_t smem, const char* name) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        int occ = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, nw * 32, smem);
+        const int grid = sms * occ;
+        for (int w = 0; w < 3; ++w) kern<<<grid, nw * 32, smem>>>(n_rows, n_per, out, 7);
+        cudaEventRecord(e0);
+        for (int w = 0; w < 10; ++w) kern<<<grid, nw * 32, smem>>>(n_rows, n_per, out, 7 + w);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        ms /= 10;
+        printf("%-34s occ %d x %2d warps  %.3f ms  %.0f GB/s  %.1f G values/s  (%s)\n", name, occ, nw, ms,
+               n_rows * n_per * 8.0 / ms / 1e6, n_rows * n_per / ms / 1e6, cudaGetErrorString(cudaGetLastError()));
+    };
+    runl(k_lanebulk<16, 8>, 8, 8 * 32 * (2 * 16 * 8 + 16), "lane bulk 128 B, 8 warps");
+    runl(k_lanebulk<32, 8>, 8, 8 * 32 * (2 * 32 * 8 + 16), "lane bulk 256 B, 8 warps");
+    runl(k_lanebulk<32, 12>, 12, 12 * 32 * (2 * 32 * 8 + 16), "lane bulk 256 B, 12 warps");
+    runl(k_lanebulk<32, 4>, 4, 4 * 32 * (2 * 32 * 8 + 16), "lane bulk 256 B, 4-warp blocks");
+    runl(k_lanebulk<64, 4>, 4, 4 * 32 * (2 * 64 * 8 + 16), "lane bulk 512 B, 4-warp blocks");
     // table gathers
     std::vector<ulonglong2> h(128);
     for (int i = 0; i < 128; ++i) h[i] = make_ulonglong2(i * 0x9E3779B97F4A7C15ULL, i);
