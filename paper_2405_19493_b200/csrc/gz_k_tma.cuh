@@ -51,6 +51,34 @@ __device__ __forceinline__ void tma_store_tile(const CUtensorMap* tm, uint32_t s
                  : "memory");
 }
 
+/* TMA tensor load of one box into shared memory, completing on an mbarrier */
+__device__ __forceinline__ void tma_load_tile(const CUtensorMap* tm, uint32_t dst, uint32_t mbar, int c0, int r0)
+{
+    asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+                 ::"r"(dst), "l"(tm), "r"(c0), "r"(r0), "r"(mbar)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_init(uint32_t mbar, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(mbar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t mbar, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint32_t mbar, uint32_t parity)
+{
+    uint32_t ok;
+    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                 : "=r"(ok)
+                 : "r"(mbar), "r"(parity)
+                 : "memory");
+    return ok != 0;
+}
+/* all but the N most recent bulk groups of this thread have completed (writes performed) */
+template <int N>
+__device__ __forceinline__ void tma_wait_done_but() { asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory"); }
+
 __device__ __forceinline__ void tma_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void tma_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void tma_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
@@ -211,11 +239,24 @@ __device__ __forceinline__ void tma_fold(uint64_t zb, uint64_t& ck, double& a1, 
     a4 = __fma_rn(z2, z2, a4);
 }
 
-template <int SRC, bool MOD, bool STATS, int NW, int NT, int FL, int TMA_K>
+/*
+ * EPI_MUTATE (config 5, x += sigma * z over every gene of `generations`
+ * generations, samplers.py:195-200): the ring tiles are first filled with x by TMA
+ * tensor LOADS (an mbarrier per ring slot; a lane writes a tile only after the
+ * warp has seen its load complete), a commit replaces the slot's x with
+ * x + sigma * z (two roundings), and the flush stores the tile back.  A row of the
+ * warp's column sequence is generations x n_genes columns; generation g + 1 reads
+ * a gene block that generation g stored n_genes/16 tiles earlier, so before every
+ * load the lane that issues them waits until all but its 7 most recent stores have
+ * completed (needs n_genes >= 16 (NT + 8)).
+ */
+template <int SRC, bool MOD, bool STATS, int NW, int NT, int FL, int TMA_K, int EPI = EPI_STORE>
 __global__ void __launch_bounds__(NW * 32, 1) k_zig_tma(const __grid_constant__ LaneParams p,
                                                         const __grid_constant__ CUtensorMap tm)
 {
     constexpr int NL = MOD ? 256 : 128;
+    constexpr bool MUT = EPI == EPI_MUTATE;
+    static_assert(!MUT || (SRC == 1 && !MOD && !STATS && FL == 1), "mutation: SplitMix64, original ziggurat");
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     const uint32_t raw_sh = sh_addr(smem_raw);
     const uint32_t base_sh = (raw_sh + 1023u) & ~1023u;            /* SWIZZLE_128B tiles: 1 KiB aligned */
@@ -225,10 +266,14 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_tma(const __grid_constant__ 
     ulonglong2* s_kw = reinterpret_cast<ulonglong2*>(base + RING);
     float2* s_yf = reinterpret_cast<float2*>(base + RING + NL * 16 * TMA_REP);
     ulonglong2* s_jump = reinterpret_cast<ulonglong2*>(base + RING + NL * 16 * TMA_REP + NL * 8);
+    /* EPI_MUTATE: one mbarrier per ring slot of each warp, after the tables */
+    const uint32_t mbar_sh = base_sh + RING + NL * 16 * TMA_REP + NL * 8;
     for (int j = threadIdx.x; j < NL * TMA_REP; j += blockDim.x) s_kw[j] = p.kw[j / TMA_REP];
     for (int j = threadIdx.x; j < NL; j += blockDim.x) s_yf[j] = p.yf[j];
     /* LCG: (A, C) of 2n steps, n <= TMA_K (the state after n draws from a round's start) */
     if (SRC == 0 && threadIdx.x <= TMA_K) s_jump[threadIdx.x] = make_ulonglong2(c_lcgA[2 * threadIdx.x], c_lcgC[2 * threadIdx.x]);
+    if (MUT && threadIdx.x < NW * NT) mbar_init(mbar_sh + 8 * threadIdx.x, 1);
+    if constexpr (MUT) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncthreads();
 
     const int lane = threadIdx.x & 31;
@@ -260,8 +305,11 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_tma(const __grid_constant__ 
        row, so a lane that finishes a row starts its next row at once instead of
        waiting at the row end for the slowest lane of the warp. */
     const int64_t g0 = (int64_t)blockIdx.x * NW + wib;
+    const uint32_t my_mbar = mbar_sh + 8 * NT * wib;
     if (g0 < n_groups) {
-        const int rowlen = (n_per + 15) & ~15;
+        /* a mutation row is every generation of one individual (n_per % 16 == 0) */
+        const int rowlen = MUT ? n_per * p.generations : (n_per + 15) & ~15;
+        const int n_row = MUT ? rowlen : n_per;       /* deviates per row */
         const int ng = (int)((n_groups - g0 + gstride - 1) / gstride);
         const int wtot = ng * rowlen;                 /* ring columns of this warp */
         const uint32_t c_end = tma_cenc(wtot);
@@ -274,11 +322,42 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_tma(const __grid_constant__ 
         uint32_t tb = 0;              /* NT == 3: byte offset of C's ring tile */
         uint32_t rej = 0, c_rej = 0xffffffffu;
         int flushed = 0;                                          /* columns handed to TMA (warp-uniform) */
-        int fk = 0, fcol = 0;                                     /* the flush position: row, column */
+        int fk = 0, fcol = 0, fgene = 0;                          /* the flush position: row, column, gene */
         uint32_t c_lim = tma_cenc(min(wtot, NT * 16));            /* nothing in flight yet: the whole ring */
         uint32_t c_limr = 0;                                      /* min(c_lim, c_rowend) */
         uint64_t ck = 0;
         double a1 = 0.0, a2 = 0.0, a3 = 0.0, a4 = 0.0;
+        double sig = 0.0;                                         /* EPI_MUTATE: the row's sigma */
+        /* EPI_MUTATE: x tiles loaded ahead (issued / seen complete by every lane) and the
+           load position (row, gene column) of the next one */
+        int ld_issued = 0, ld_ready = 0, lk = 0, lcol = 0, lgene = 0;
+        auto issue_loads = [&](int upto) {
+            /* lane 0 only: loads of tiles [ld_issued, upto) into their (free) ring slots */
+            while (ld_issued < upto && ld_issued * 16 < wtot) {
+                tma_wait_done_but<7>();   /* the previous generation's store of this gene block */
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+                const int sl = slot_of(ld_issued);
+                mbar_expect_tx(my_mbar + 8 * sl, TMA_TILE_BYTES);
+                tma_load_tile(&tm, wring + sl * TMA_TILE_BYTES, my_mbar + 8 * sl, lgene,
+                              (int)((g0 + (int64_t)lk * gstride) * 32));
+                ++ld_issued;
+                lgene += 16;
+                if (lgene >= n_per) lgene = 0;
+                lcol += 16;
+                if (lcol >= rowlen) {
+                    lcol = 0;
+                    ++lk;
+                }
+            }
+        };
+        if constexpr (MUT) {
+            if (lane == 0) issue_loads(NT);
+            __syncwarp();
+            ld_issued = __shfl_sync(GZ_FULL, ld_issued, 0);
+            lk = __shfl_sync(GZ_FULL, lk, 0);
+            lcol = __shfl_sync(GZ_FULL, lcol, 0);
+            lgene = __shfl_sync(GZ_FULL, lgene, 0);
+        }
 
         /* row transitions (divergent, once per row and lane): store the finished
            row's state, load the next row's */
@@ -305,7 +384,8 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_tma(const __grid_constant__ 
                             gam = p.state_in[2 * sid + 1];
                         }
                         C = tma_cenc(k * rowlen);
-                        c_rowend = tma_cenc(k * rowlen + n_per);
+                        c_rowend = tma_cenc(k * rowlen + n_row);
+                        if constexpr (MUT) sig = p.sigma[sid];
                         if constexpr (NT == 3) tb = (uint32_t)slot_of((k * rowlen) >> 4) * TMA_TILE_BYTES;
                     } else {
                         C = c_rowend = tma_cenc((k + 1) * rowlen);   /* no stream: skip the row */
@@ -318,6 +398,15 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_tma(const __grid_constant__ 
             c_limr = min(c_lim, c_rowend);
         };
         next_rows();
+        /* EPI_MUTATE: tiles whose x load every lane has seen complete */
+        auto poll_loads = [&]() {
+            int r = ld_ready;
+            while (r < ld_issued && mbar_try_wait(my_mbar + 8 * slot_of(r), (uint32_t)(r / NT) & 1u)) ++r;
+            ld_ready = (int)__reduce_min_sync(GZ_FULL, (unsigned)r);
+            c_lim = tma_cenc(min(min(wtot, flushed + SLACK), 16 * ld_ready));
+            c_limr = min(c_lim, c_rowend);
+        };
+        if constexpr (MUT) poll_loads();
 
         while (true) {
             /* ---- one round: TMA_K attempts per lane, no branches ---- */
@@ -344,7 +433,14 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_tma(const __grid_constant__ 
                 GZ_CHECK(!commit || (a >= wring && a < wring + NT * TMA_TILE_BYTES), a - wring);
                 GZ_CHECK(!commit || tma_cdec(C) < flushed + SLACK + FB, tma_cdec(C) - flushed);
                 if (commit) {
-                    asm volatile("st.shared.u64 [%0], %1;" ::"r"(a), "l"(zb) : "memory");
+                    if constexpr (MUT) {
+                        double xo;
+                        asm volatile("ld.shared.f64 %0, [%1];" : "=d"(xo) : "r"(a) : "memory");
+                        const double xn = __dadd_rn(xo, __dmul_rn(sig, __longlong_as_double((long long)zb)));
+                        asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(xn) : "memory");
+                    } else {
+                        asm volatile("st.shared.u64 [%0], %1;" ::"r"(a), "l"(zb) : "memory");
+                    }
                     C = tma_cinc(C);
                     if constexpr (NT == 3) {
                         if ((C & 0x78u) == 0) tb = tb == 2u * TMA_TILE_BYTES ? 0u : tb + TMA_TILE_BYTES;
@@ -404,7 +500,14 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_tma(const __grid_constant__ 
                         GZ_CHECK(C < c_limr, tma_cdec(C));
                         const uint64_t zb = (uint64_t)__double_as_longlong(x) ^ sgn;
                         const uint32_t a = NT == 3 ? my_row + tb + ((C & 0x78u) ^ lx) : tma_caddr<NT>(my_row, lx, C);
-                        asm volatile("st.shared.u64 [%0], %1;" ::"r"(a), "l"(zb) : "memory");
+                        if constexpr (MUT) {
+                            double xo;
+                            asm volatile("ld.shared.f64 %0, [%1];" : "=d"(xo) : "r"(a) : "memory");
+                            const double xn = __dadd_rn(xo, __dmul_rn(sig, __longlong_as_double((long long)zb)));
+                            asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(xn) : "memory");
+                        } else {
+                            asm volatile("st.shared.u64 [%0], %1;" ::"r"(a), "l"(zb) : "memory");
+                        }
                         C = tma_cinc(C);
                         if constexpr (NT == 3) {
                             if ((C & 0x78u) == 0) tb = tb == 2u * TMA_TILE_BYTES ? 0u : tb + TMA_TILE_BYTES;
@@ -471,9 +574,11 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_tma(const __grid_constant__ 
                     for (int j = 0; j < FL; ++j) {
                         if (16 * j < cnt)
                             tma_store_tile(&tm, wring + slot_of((flushed >> 4) + j) * TMA_TILE_BYTES,
-                                           fcol + 16 * j, (int)((g0 + (int64_t)fk * gstride) * 32));
+                                           (MUT ? fgene : fcol) + 16 * j, (int)((g0 + (int64_t)fk * gstride) * 32));
                     }
                     tma_commit();
+                    /* EPI_MUTATE: the slot freed by the wait above takes the x tile NT - 1 ahead */
+                    if constexpr (MUT) issue_loads((flushed >> 4) + NT);
                 }
                 __syncwarp();
                 flushed += cnt;
@@ -482,9 +587,19 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_tma(const __grid_constant__ 
                     fcol = 0;
                     ++fk;
                 }
+                if constexpr (MUT) {
+                    fgene += cnt;
+                    if (fgene >= n_per) fgene = 0;
+                    ld_issued = __shfl_sync(GZ_FULL, ld_issued, 0);
+                    lk = __shfl_sync(GZ_FULL, lk, 0);
+                    lcol = __shfl_sync(GZ_FULL, lcol, 0);
+                    lgene = __shfl_sync(GZ_FULL, lgene, 0);
+                }
                 c_lim = tma_cenc(min(wtot, flushed + SLACK));   /* the tiles of the block just freed */
+                if constexpr (MUT) c_lim = min(c_lim, tma_cenc(min(wtot, 16 * ld_ready)));
                 c_limr = min(c_lim, c_rowend);
             }
+            if constexpr (MUT) poll_loads();
             if (minw >= wtot) break;   /* every row complete and handed to TMA */
         }
         if (lane == 0) tma_wait_all();

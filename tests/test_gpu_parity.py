@@ -311,7 +311,9 @@ def test_config5_mutation(golden):
 
 
 @pytest.mark.parametrize("n,genes,gens,pad", [(100, 32, 3, 0), (2011, 48, 2, 0), (700, 64, 5, 2), (333, 1024, 2, 0),
-                                              (97, 96, 3, 1), (64, 40, 2, 0), (40, 16, 4, 0)])
+                                              (97, 96, 3, 1), (64, 40, 2, 0), (40, 16, 4, 0),
+                                              (2011, 192, 3, 0), (1000, 256, 2, 4), (40000, 192, 2, 0),
+                                              (70, 400, 1, 2)])
 def test_mutate_vs_oracle(n, genes, gens, pad, policy):
     """gz_mutate on both kernel families: rows of any length, strided (pad) and
     8-byte-aligned-only (odd ld) rows, several generations per launch."""

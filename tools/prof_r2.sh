@@ -14,9 +14,18 @@ python bench.py --impl reference --steps 3 --warmup 1 > $O/bench_ref.json 2>$O/b
 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file $O/launches.csv python bench.py --steps 5 --warmup 3 --no-cpu --no-e2e > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k_zig_tma -s 3 -c 1 -o $O/c4_k_zig_tma python bench.py --steps 1 --warmup 3 --no-extra --no-cpu --no-e2e > /dev/null 2>&1
 else
-python tools/prof_one.py c3 0 1 && ncu --set full --clock-control none --import-source on -k regex:k_zig_tma -c 1 -o $O/c3_k_zig_tma python tools/prof_one.py c3 0 1 > /dev/null 2>&1
-python tools/prof_one.py c2 0 1 && ncu --set full --clock-control none --import-source on -k regex:k_polar_q -c 1 -o $O/c2_k_polar_q python tools/prof_one.py c2 0 1 > /dev/null 2>&1
-python tools/prof_one.py c5 0 1 && ncu --set full --clock-control none --import-source on -k regex:k_zig_lane -c 1 -o $O/c5_k_zig_lane_mutate python tools/prof_one.py c5 0 1 > /dev/null 2>&1
-python tools/prof_one.py c1 0 1 && ncu --set full --clock-control none --import-source on -k regex:k_zig -c 1 -o $O/c1_k_zig_lseg python tools/prof_one.py c1 0 1 > /dev/null 2>&1
+# summaries are made on the box and the reports dropped (gpurun brings back <= 64 MiB)
+cap() {  # cap NAME KERNEL_REGEX CFG
+  python tools/prof_one.py $3 0 1 > /dev/null && ncu --set full --clock-control none --import-source on -k regex:$2 -c 1 -o $O/$1 python tools/prof_one.py $3 0 1 > /dev/null 2>&1
+  python tools/ncu_summary.py $O/$1.ncu-rep > $O/${1}_summary.txt
+  ncu -i $O/$1.ncu-rep --page source --print-source sass --csv > $O/$1_src.csv 2>/dev/null
+  python tools/sass_hot.py $O/$1_src.csv 30 > $O/${1}_sass_hot.txt
+  python tools/sass_blocks.py $O/$1_src.csv 0.004 > $O/${1}_blocks.txt
+  rm -f $O/$1.ncu-rep $O/$1_src.csv
+}
+cap c3_k_zig_tma k_zig_tma c3
+cap c2_k_polar_q k_polar_q c2
+cap c5_k_zig_tma_mutate k_zig_tma c5
+cap c1_k_zig_lseg k_zig_lseg c1
 fi
 ls -la $O
