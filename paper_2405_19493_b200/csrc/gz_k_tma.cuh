@@ -331,6 +331,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_tma(const __grid_constant__ 
         /* EPI_MUTATE: x tiles loaded ahead (issued / seen complete by every lane) and the
            load position (row, gene column) of the next one */
         int ld_issued = 0, ld_ready = 0, lk = 0, lcol = 0, lgene = 0;
+        bool just_flushed = false;   /* a store left this round: its slot is reloaded next round */
         auto issue_loads = [&](int upto) {
             /* lane 0 only: loads of tiles [ld_issued, upto) into their (free) ring slots */
             while (ld_issued < upto && ld_issued * 16 < wtot) {
@@ -353,10 +354,6 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_tma(const __grid_constant__ 
         if constexpr (MUT) {
             if (lane == 0) issue_loads(NT);
             __syncwarp();
-            ld_issued = __shfl_sync(GZ_FULL, ld_issued, 0);
-            lk = __shfl_sync(GZ_FULL, lk, 0);
-            lcol = __shfl_sync(GZ_FULL, lcol, 0);
-            lgene = __shfl_sync(GZ_FULL, lgene, 0);
         }
 
         /* row transitions (divergent, once per row and lane): store the finished
@@ -400,10 +397,20 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_tma(const __grid_constant__ 
         next_rows();
         /* EPI_MUTATE: tiles whose x load every lane has seen complete */
         auto poll_loads = [&]() {
+            /* loads go only into slots whose store has been read, so the loaded tiles are
+               exactly the writable ones */
+            if (lane == 0 && !just_flushed && ld_issued < (flushed >> 4) + NT && ld_issued * 16 < wtot) {
+                tma_wait_read_all();   /* the last store (issued a round ago) has been read */
+                issue_loads((flushed >> 4) + NT);
+            }
+            ld_issued = __shfl_sync(GZ_FULL, ld_issued, 0);
+            lk = __shfl_sync(GZ_FULL, lk, 0);
+            lcol = __shfl_sync(GZ_FULL, lcol, 0);
+            lgene = __shfl_sync(GZ_FULL, lgene, 0);
             int r = ld_ready;
             while (r < ld_issued && mbar_try_wait(my_mbar + 8 * slot_of(r), (uint32_t)(r / NT) & 1u)) ++r;
             ld_ready = (int)__reduce_min_sync(GZ_FULL, (unsigned)r);
-            c_lim = tma_cenc(min(min(wtot, flushed + SLACK), 16 * ld_ready));
+            c_lim = tma_cenc(min(wtot, 16 * ld_ready));
             c_limr = min(c_lim, c_rowend);
         };
         if constexpr (MUT) poll_loads();
@@ -432,19 +439,23 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_tma(const __grid_constant__ 
                 GZ_CHECK(ioff < NL * 128u, ioff);
                 GZ_CHECK(!commit || (a >= wring && a < wring + NT * TMA_TILE_BYTES), a - wring);
                 GZ_CHECK(!commit || tma_cdec(C) < flushed + SLACK + FB, tma_cdec(C) - flushed);
-                if (commit) {
-                    if constexpr (MUT) {
-                        double xo;
-                        asm volatile("ld.shared.f64 %0, [%1];" : "=d"(xo) : "r"(a) : "memory");
-                        const double xn = __dadd_rn(xo, __dmul_rn(sig, __longlong_as_double((long long)zb)));
-                        asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(xn) : "memory");
-                    } else {
-                        asm volatile("st.shared.u64 [%0], %1;" ::"r"(a), "l"(zb) : "memory");
-                    }
-                    C = tma_cinc(C);
-                    if constexpr (NT == 3) {
-                        if ((C & 0x78u) == 0) tb = tb == 2u * TMA_TILE_BYTES ? 0u : tb + TMA_TILE_BYTES;
-                    }
+                /* EPI_MUTATE: the slot's x is read whether or not the attempt commits (the
+                   address is inside the ring either way), so only the store is predicated */
+                uint64_t sv = zb;
+                if constexpr (MUT) {
+                    double xo;
+                    asm("ld.shared.f64 %0, [%1];" : "=d"(xo) : "r"(a));
+                    sv = (uint64_t)__double_as_longlong(__dadd_rn(xo, __dmul_rn(sig, __longlong_as_double((long long)zb))));
+                }
+                if (commit) asm volatile("st.shared.u64 [%0], %1;" ::"r"(a), "l"(sv) : "memory");
+                if constexpr (NT == 3) {
+                    /* three tiles: advance the tile offset (branch-free) when the column wraps */
+                    const uint32_t cn = tma_cinc(C);
+                    const uint32_t tn = tb == 2u * TMA_TILE_BYTES ? 0u : tb + TMA_TILE_BYTES;
+                    tb = (commit && (cn & 0x78u) == 0) ? tn : tb;
+                    C = commit ? cn : C;
+                } else {
+                    C = commit ? tma_cinc(C) : C;
                 }
             }
             /* the live attempts are a prefix of the round: the committed ones plus a
@@ -518,6 +529,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_tma(const __grid_constant__ 
             next_rows();
             /* ---- hand complete blocks of FB columns to TMA ---- */
             const int minw = tma_cdec(__reduce_min_sync(GZ_FULL, C));
+            just_flushed = false;
             while (minw - flushed >= FB || (minw >= wtot && flushed < wtot)) {
                 const int cnt = min(FB, wtot - flushed);
                 GZ_CHECK(cnt > 0 && flushed + cnt <= minw && fk < ng && fcol < rowlen, fcol);
@@ -577,8 +589,6 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_tma(const __grid_constant__ 
                                            (MUT ? fgene : fcol) + 16 * j, (int)((g0 + (int64_t)fk * gstride) * 32));
                     }
                     tma_commit();
-                    /* EPI_MUTATE: the slot freed by the wait above takes the x tile NT - 1 ahead */
-                    if constexpr (MUT) issue_loads((flushed >> 4) + NT);
                 }
                 __syncwarp();
                 flushed += cnt;
@@ -590,14 +600,11 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_tma(const __grid_constant__ 
                 if constexpr (MUT) {
                     fgene += cnt;
                     if (fgene >= n_per) fgene = 0;
-                    ld_issued = __shfl_sync(GZ_FULL, ld_issued, 0);
-                    lk = __shfl_sync(GZ_FULL, lk, 0);
-                    lcol = __shfl_sync(GZ_FULL, lcol, 0);
-                    lgene = __shfl_sync(GZ_FULL, lgene, 0);
+                    just_flushed = true;
+                } else {
+                    c_lim = tma_cenc(min(wtot, flushed + SLACK));   /* the tiles of the block just freed */
+                    c_limr = min(c_lim, c_rowend);
                 }
-                c_lim = tma_cenc(min(wtot, flushed + SLACK));   /* the tiles of the block just freed */
-                if constexpr (MUT) c_lim = min(c_lim, tma_cenc(min(wtot, 16 * ld_ready)));
-                c_limr = min(c_lim, c_rowend);
             }
             if constexpr (MUT) poll_loads();
             if (minw >= wtot) break;   /* every row complete and handed to TMA */
