@@ -378,13 +378,13 @@ def _numba_worker(args):
 
 def reference_as_is(n_streams=NUMBA_SAMPLE_STREAMS):
     """The reference's own numba engine.fill_gaussians per stream (baseline/_ref), fanned
-    out over P = cpu_count worker processes each owning a contiguous block of streams
-    (the reference itself is single-threaded).  None when baseline/_ref is absent."""
+    out over P = min(cpu_count, 32) worker processes each owning a contiguous block of
+    streams (the reference itself is single-threaded).  None when baseline/_ref is absent."""
     if not os.path.isdir(os.path.join(ROOT, "baseline", "_ref", "gausszig")):
         return None
     import multiprocessing as mp
 
-    P = os.cpu_count() or 1
+    P = min(os.cpu_count() or 1, 32)   # each worker JIT-compiles the numba engine
     per = (n_streams + P - 1) // P
     jobs = [(k * per, min(per, n_streams - k * per), N_PER, os.path.join("/tmp", "gz_numba_cache"))
             for k in range(P) if k * per < n_streams]
