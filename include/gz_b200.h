@@ -69,8 +69,9 @@ int gz_device_count(void);
  * Kernel family for gz_fill_gaussians on the current device: 0 = automatic
  * (one lane per stream from 32768 streams up, one warp per stream below),
  * 1 = always one warp per stream (jump-ahead decode), 2 = always one lane per
- * stream (ziggurat rows leave through TMA tensor stores where the row layout
- * allows), 3 = one lane per stream with the shared-ring lane stores only.
+ * stream (ziggurat rows leave through lane-private 32-byte stores where the row
+ * layout allows, else TMA tensor stores), 3 = one lane per stream with the
+ * shared-ring lane stores only, 4 = one lane per stream with TMA tensor stores.
  * Results are identical; this only selects the schedule.
  */
 int gz_set_kernel_policy(int policy);

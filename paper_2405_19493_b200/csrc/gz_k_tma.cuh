@@ -43,6 +43,17 @@
 constexpr int TMA_TILE_BYTES = 32 * 128;
 constexpr int TMA_REP = 8;             /* replicas of the layer rows */
 constexpr uint64_t GZ_LCG_AINV = 0xDFE05BCB1365ULL;   /* 0x5DEECE66D^-1 mod 2^48 */
+constexpr size_t TMA_SMEM_MAX = 232448;   /* sm_100 opt-in dynamic shared memory per block */
+
+/* dynamic shared memory of k_zig_tma without the ring alignment slack */
+__host__ __device__ constexpr size_t tma_smem_core(int NW, int NT, int NL, int K, bool lcg) { return (size_t)NW * NT * TMA_TILE_BYTES + (size_t)NL * 16 * TMA_REP + (size_t)NL * 8 + (lcg ? 16 * (size_t)(K + 1) : 0); }
+/* a power-of-two ring whose base fits 16 KiB alignment: a slot address is one LOP3 */
+__host__ __device__ constexpr bool tma_align16(int NW, int NT, int NL, int K, bool lcg, bool mut) { return !mut && (NT & (NT - 1)) == 0 && tma_smem_core(NW, NT, NL, K, lcg) + 16384 <= TMA_SMEM_MAX; }
+__host__ __device__ constexpr size_t tma_smem_bytes(int NW, int NT, int NL, int K, bool lcg, bool mut) { return tma_smem_core(NW, NT, NL, K, lcg) + (tma_align16(NW, NT, NL, K, lcg, mut) ? 16384 : 1024); }
+
+#ifndef TMA_CHV
+#define TMA_CHV 1
+#endif
 
 __device__ __forceinline__ void tma_store_tile(const CUtensorMap* tm, uint32_t src, int c0, int r0)
 {
@@ -87,6 +98,12 @@ __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.a
 __device__ __forceinline__ void lds_u64x2_v(uint32_t a, uint64_t& x, uint64_t& y)
 {
     asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(x), "=l"(y) : "r"(a));
+}
+/* a gather from a read-only table (layer rows, jump constants): not volatile, so the
+   compiler may hoist it past the ring stores of earlier attempts */
+__device__ __forceinline__ void lds_tab(uint32_t a, uint64_t& x, uint64_t& y)
+{
+    asm("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(x), "=l"(y) : "r"(a));
 }
 
 /* one draw of the stream: `t` is the draw cursor (LCG: the unmasked 48-bit
@@ -151,6 +168,7 @@ __device__ __forceinline__ void lcg_step32(uint32_t l, uint32_t h, uint32_t& ol,
 template <int SRC>
 struct TmaCursor {
     uint32_t lo, hi;
+    __device__ __forceinline__ TmaCursor() : lo(0), hi(0) {}
     __device__ __forceinline__ explicit TmaCursor(uint64_t s) : lo((uint32_t)s), hi((uint32_t)(s >> 32)) {}
     __device__ __forceinline__ uint64_t state() const { return ((uint64_t)hi << 32) | lo; }
     __device__ __forceinline__ void draw(uint64_t gam, uint64_t inc2, uint32_t& uhi, uint32_t& ulo)
@@ -259,7 +277,9 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_tma(const __grid_constant__ 
     static_assert(!MUT || (SRC == 1 && !MOD && !STATS && FL == 1), "mutation: SplitMix64, original ziggurat");
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     const uint32_t raw_sh = sh_addr(smem_raw);
-    const uint32_t base_sh = (raw_sh + 1023u) & ~1023u;            /* SWIZZLE_128B tiles: 1 KiB aligned */
+    /* SWIZZLE_128B tiles: 1 KiB aligned; the UNCOND rounds need the ring 16 KiB aligned */
+    constexpr bool ALIGN16 = tma_align16(NW, NT, NL, TMA_K, SRC == 0, MUT);
+    const uint32_t base_sh = ALIGN16 ? ((raw_sh + 16383u) & ~16383u) : ((raw_sh + 1023u) & ~1023u);
     unsigned char* base = smem_raw + (base_sh - raw_sh);
     constexpr uint32_t RING = NW * NT * TMA_TILE_BYTES;
     const uint32_t kw_sh = base_sh + RING;
@@ -281,6 +301,10 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_tma(const __grid_constant__ 
     const uint32_t wring = base_sh + wib * NT * TMA_TILE_BYTES;
     const uint32_t my_row = wring + lane * 128;
     const uint32_t lx = (uint32_t)(lane & 7) << 4;                  /* the row's swizzle */
+    /* UNCOND rounds: with the ring base 16 KiB aligned (ALIGN16) my_row has no bit in the
+       tile|column mask, so a slot address is ((C & mask) ^ rowx), one LOP3 */
+    constexpr bool UNCOND = !MUT && (NT & (NT - 1)) == 0;
+    const uint32_t rowx = my_row ^ lx;
     const uint32_t my_kw = kw_sh + lx;                              /* replica lane & 7 */
     const uint32_t yf_sh = sh_addr(s_yf);
     const uint32_t jump_sh = sh_addr(s_jump);
@@ -288,6 +312,13 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_tma(const __grid_constant__ 
        addend would split every IMAD.WIDE.U32 into a multiply and a 64-bit add) */
     const uint64_t lcg_inc = SRC == 0 ? ld_keep(&c_lcgC[1]) : 0;
     const uint64_t lcg_inc2 = SRC == 0 ? ld_keep(&c_lcgC[2]) : 0;
+    /* LCG draw chains of the UNCOND rounds: (A, C) of 2 (TMA_K / CH) j steps */
+    uint64_t jA[TMA_CHV > 1 ? TMA_CHV : 1], jC[TMA_CHV > 1 ? TMA_CHV : 1];
+#pragma unroll
+    for (int j = 0; j < (TMA_CHV > 1 ? TMA_CHV : 1); ++j) {
+        jA[j] = (SRC == 0 && j > 0) ? ld_keep(&c_lcgA[2 * (TMA_K / TMA_CHV) * j]) : 0;
+        jC[j] = (SRC == 0 && j > 0) ? ld_keep(&c_lcgC[2 * (TMA_K / TMA_CHV) * j]) : 0;
+    }
     const int n_per = p.n_per;
     const uint32_t guard32 = p.guard > 0xffffffffll ? 0xffffffffu : (uint32_t)p.guard;
     const int64_t n_streams = p.n_streams;
@@ -325,6 +356,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_tma(const __grid_constant__ 
         int fk = 0, fcol = 0, fgene = 0;                          /* the flush position: row, column, gene */
         uint32_t c_lim = tma_cenc(min(wtot, NT * 16));            /* nothing in flight yet: the whole ring */
         uint32_t c_limr = 0;                                      /* min(c_lim, c_rowend) */
+        uint32_t c_ring = tma_cenc(NT * 16);                      /* UNCOND: ring room, not capped at wtot */
         uint64_t ck = 0;
         double a1 = 0.0, a2 = 0.0, a3 = 0.0, a4 = 0.0;
         double sig = 0.0;                                         /* EPI_MUTATE: the row's sigma */
@@ -420,6 +452,54 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_tma(const __grid_constant__ 
             bool frozen = false;
             const uint32_t C0 = C;
             TmaCursor<SRC> t(S);
+            if constexpr (UNCOND) {
+                /* every attempt's deviate goes to slot C0 + k unconditionally (the slots past the
+                   committed prefix are rewritten later); the committed attempts are the leading
+                   fast accepts, capped at the row end.  A lane writes only when the whole round
+                   fits the ring room (act), so no slot of a tile in flight is touched. */
+                const bool act = C0 < c_rowend && ((C0 + 8u * TMA_K) | 0xF80u) <= c_ring;
+                uint32_t fm = 0;
+                /* LCG: CH independent draw chains (chain j starts 2 KC j steps ahead by one jump),
+                   so the attempts of different chains do not wait for each other */
+                constexpr int CH = (SRC == 0 && TMA_K % TMA_CHV == 0) ? TMA_CHV : 1, KC = TMA_K / CH;
+                static_assert(TMA_K % CH == 0, "chains split the round evenly");
+                TmaCursor<SRC> tcs[CH] = {t};
+#pragma unroll
+                for (int j = 1; j < CH; ++j) tcs[j] = TmaCursor<SRC>(S * jA[j] + jC[j]);
+                /* stores after the last attempt (see k_zig_lst: a table gather may not pass a
+                   shared store in program order) */
+                uint64_t zbs[TMA_K];
+#pragma unroll
+                for (int kk2 = 0; kk2 < TMA_K; ++kk2) {
+                    uint32_t uhi, ulo;
+                    tcs[kk2 / KC].draw(gam, lcg_inc2, uhi, ulo);
+                    uint32_t ioff, mhi, mlo, sgn;
+                    tma_split32<MOD>(uhi, ulo, ioff, mhi, mlo, sgn);
+                    uint64_t kk, wb;
+                    lds_tab(my_kw + ioff, kk, wb);
+                    const uint64_t m = ((uint64_t)mhi << 32) | mlo;
+                    const double x = __dmul_rn(__ull2double_rn(m), __longlong_as_double((long long)wb));
+                    if (m < kk) fm |= 1u << kk2;
+                    zbs[kk2] = (uint64_t)__double_as_longlong(x) ^ ((uint64_t)sgn << 32);
+                    GZ_CHECK(ioff < NL * 128u, ioff);
+                }
+                if (act) {
+#pragma unroll
+                    for (int kk2 = 0; kk2 < TMA_K; ++kk2) {
+                        const uint32_t cm = (C0 + 8u * kk2) & (((NT - 1u) << 12) | 0x78u);
+                        const uint32_t a = ALIGN16 ? (cm ^ rowx) : (my_row + (cm ^ lx));
+                        GZ_CHECK(a == tma_caddr<NT>(my_row, lx, (C0 + 8u * kk2) | 0xF80u), a);
+                        asm volatile("st.shared.u64 [%0], %1;" ::"r"(a), "l"(zbs[kk2]) : "memory");
+                    }
+                }
+                const int lead = __ffs(~fm) - 1;   /* leading fast accepts (fm < 2^TMA_K) */
+                const uint32_t C_lead = (C0 + 8u * (uint32_t)lead) | 0xF80u;
+                if (act) {
+                    C = min(C_lead, c_rowend);
+                    frozen = C_lead < c_rowend && lead < TMA_K;
+                }
+                GZ_CHECK(!act || tma_cdec(C) <= flushed + SLACK + FB, tma_cdec(C) - flushed);
+            } else {
 #pragma unroll
             for (int kk2 = 0; kk2 < TMA_K; ++kk2) {
                 const bool live = !frozen && C < c_limr;
@@ -428,7 +508,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_tma(const __grid_constant__ 
                 uint32_t ioff, mhi, mlo, sgn;
                 tma_split32<MOD>(uhi, ulo, ioff, mhi, mlo, sgn);
                 uint64_t kk, wb;
-                lds_u64x2_v(my_kw + ioff, kk, wb);
+                lds_tab(my_kw + ioff, kk, wb);
                 const uint64_t m = ((uint64_t)mhi << 32) | mlo;
                 const double x = __dmul_rn(__ull2double_rn(m), __longlong_as_double((long long)wb));
                 const bool ok = m < kk;
@@ -458,6 +538,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_tma(const __grid_constant__ 
                     C = commit ? tma_cinc(C) : C;
                 }
             }
+            }
             /* the live attempts are a prefix of the round: the committed ones plus a
                frozen one; the state after them by jump-ahead from the round's start */
             {
@@ -465,7 +546,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_tma(const __grid_constant__ 
                 GZ_CHECK(n_live <= (uint32_t)TMA_K, n_live);
                 if constexpr (SRC == 0) {
                     uint64_t ja, jc;
-                    lds_u64x2_v(jump_sh + 16 * n_live, ja, jc);
+                    lds_tab(jump_sh + 16 * n_live, ja, jc);
                     S = S * ja + jc;
                 } else {
                     S += (uint64_t)n_live * gam;
@@ -479,7 +560,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_tma(const __grid_constant__ 
                     uint64_t m, sgn;
                     tma_split<MOD>(u, i, m, sgn);
                     uint64_t kk, wb;
-                    lds_u64x2_v(my_kw + (i << 7), kk, wb);
+                    lds_tab(my_kw + (i << 7), kk, wb);
                     double x = __dmul_rn(__ull2double_rn(m), __longlong_as_double((long long)wb));
                     bool ok;
                     if (i != 0) {
@@ -516,7 +597,8 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_tma(const __grid_constant__ 
                             asm volatile("ld.shared.f64 %0, [%1];" : "=d"(xo) : "r"(a) : "memory");
                             const double xn = __dadd_rn(xo, __dmul_rn(sig, __longlong_as_double((long long)zb)));
                             asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(xn) : "memory");
-                        } else {
+                        } else if (!UNCOND || i == 0) {
+                            /* (UNCOND: a wedge's slot already holds x, written in the round) */
                             asm volatile("st.shared.u64 [%0], %1;" ::"r"(a), "l"(zb) : "memory");
                         }
                         C = tma_cinc(C);
@@ -603,6 +685,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_tma(const __grid_constant__ 
                     just_flushed = true;
                 } else {
                     c_lim = tma_cenc(min(wtot, flushed + SLACK));   /* the tiles of the block just freed */
+                    c_ring = tma_cenc(flushed + SLACK);
                     c_limr = min(c_lim, c_rowend);
                 }
             }

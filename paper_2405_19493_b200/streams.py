@@ -97,7 +97,7 @@ def fill_gaussians_streams(sampler, source, states, out, *, spare=None, has_spar
 def set_kernel_policy(policy: str) -> None:
     """'auto', 'warp' (one warp decodes one stream) or 'lane' (one lane per stream)."""
     L = _lib.load()
-    check(L.gz_set_kernel_policy({"auto": 0, "warp": 1, "lane": 2, "lane-ring": 3}[policy]))
+    check(L.gz_set_kernel_policy({"auto": 0, "warp": 1, "lane": 2, "lane-ring": 3, "lane-tma": 4}[policy]))
 
 
 def fill_u64_streams(source, states, out, *, stream=None, sync: bool = True) -> None:

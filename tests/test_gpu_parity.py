@@ -156,7 +156,7 @@ def test_tail_sample_scripted_matches_reference(golden_cli):
 
 # ---- multi-stream hot path ------------------------------------------------------
 
-@pytest.fixture(params=["warp", "lane", "lane-ring"])
+@pytest.fixture(params=["warp", "lane", "lane-ring", "lane-tma"])
 def policy(request):
     streams.set_kernel_policy(request.param)
     yield request.param

@@ -35,7 +35,7 @@ def one_case(rng):
         n, n_per = int(rng.integers(32768, 45000)), int(rng.integers(1, 80))
     else:
         n, n_per = int(rng.integers(200, 3000)), int(rng.integers(0, 600))
-    policy = ["auto", "warp", "lane"][rng.integers(3)]
+    policy = ["auto", "warp", "lane", "lane-tma"][rng.integers(4)]
     raw = rng.integers(0, 2 ** 63, size=(n, 2), dtype=np.uint64) * np.uint64(2) + rng.integers(0, 2, size=(n, 2),
                                                                                                dtype=np.uint64)
     st_np = raw[:, 0] & np.uint64((1 << 48) - 1) if source == "lcg48" else raw.copy()
@@ -96,7 +96,7 @@ def one_case(rng):
 def mutate_case(rng):
     n, genes, gens = int(rng.integers(1, 3000)), int(rng.integers(1, 700)), int(rng.integers(1, 4))
     pad = int(rng.integers(0, 3))
-    policy = ["auto", "warp", "lane"][rng.integers(3)]
+    policy = ["auto", "warp", "lane", "lane-tma"][rng.integers(4)]
     st_np = rng.integers(0, 2 ** 63, size=(n, 2), dtype=np.uint64)
     st_np[:, 1] |= np.uint64(1)
     x_np = rng.standard_normal((n, genes))

@@ -1,0 +1,5 @@
+# ring stores after the attempts (LDS batched): k_zig_lst 16 warps (DADD cvt / I2F), 20 warps; k_zig_tma
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "test_random_streams_vs_oracle and lane" 2>&1 | tail -2
+echo "== l16"; GZ_POLICY=lane timeout 300 python tools/quick_time.py c4 c4s c3 | grep -v policy
+for v in l16i l20i; do echo "== $v"; GZ_POLICY=lane GZ_LIB=build/var/$v/libgzb200.so timeout 300 python tools/quick_time.py c4 c4s c3 2>&1 | grep -v policy; done
+echo "== tma"; GZ_POLICY=lane-tma timeout 300 python tools/quick_time.py c4 c4s c3 | grep -v policy
