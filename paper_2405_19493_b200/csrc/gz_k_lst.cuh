@@ -35,6 +35,9 @@
 #pragma once
 
 constexpr int LST_SLOTS = 16;   /* staging slots per lane (8 bytes each) */
+#ifndef LST_EXP
+#define LST_EXP 0
+#endif
 #ifndef LST_CVT
 #define LST_CVT 0
 #endif
@@ -109,12 +112,17 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ 
     uint64_t ck = 0;
     double a1 = 0.0, a2 = 0.0, a3 = 0.0, a4 = 0.0;
 
+    /* consecutive rows of a lane are sstride streams apart: stream, row and state
+       pointers advance by constant strides (no 64-bit multiplies per row) */
+    const int64_t sstride = gstride * 32;
+    const int64_t last = n_streams - 1;
+    sid = g0 * 32 + lane - sstride;
+    double* rowp_next = p.out + (g0 * 32 + lane) * p.ld;
+    const int64_t rstride = sstride * p.ld;
     /* the next row's state, loaded a row ahead (clamped to a valid stream, so the load is
        unconditional and lands in its own registers) */
-    auto load_state = [&](int kk, uint64_t& s, uint64_t& g) {
-        if (ng == 0) return;
-        int64_t q = (g0 + (int64_t)min(kk, ng - 1) * gstride) * 32 + lane;
-        if (q >= n_streams) q = n_streams - 1;
+    auto load_state = [&](int64_t q, uint64_t& s, uint64_t& g) {
+        if (q > last) q = last;
         if constexpr (SRC == 0) {
             s = ld_keep(p.state_in + q);
         } else {
@@ -126,52 +134,51 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ 
     auto next_row = [&]() {
         while (C >= c_rowend && k < ng) {
             if (valid && !failed) {
-                /* the row's last partial chunk, its witnesses and its final state */
-                for (; f < c_rowend; ++f) {
-                    uint64_t v;
-                    asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(((f << 3) & 0x78u) ^ rowx));
-                    rowp[f - c_row0] = __longlong_as_double((long long)v);
-                    if constexpr (STATS) tma_fold(v, ck, a1, a2, a3, a4);
+                if (n_per & 3) {
+                    /* the row's last partial chunk */
+                    for (; f < c_rowend; ++f) {
+                        uint64_t v;
+                        asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(((f << 3) & 0x78u) ^ rowx));
+                        rowp[f - c_row0] = __longlong_as_double((long long)v);
+                        if constexpr (STATS) tma_fold(v, ck, a1, a2, a3, a4);
+                    }
                 }
+                /* its witnesses and its final state */
                 if constexpr (STATS) {
                     if (p.checksum) p.checksum[sid] = ck;
                     if (p.psum) {
-                        p.psum[4 * sid + 0] = a1;
-                        p.psum[4 * sid + 1] = a2;
-                        p.psum[4 * sid + 2] = a3;
-                        p.psum[4 * sid + 3] = a4;
+                        double* ps = p.psum + 4 * sid;   /* 16-byte aligned (lst_eligible) */
+                        asm volatile("st.global.v2.f64 [%0], {%1, %2};" ::"l"(ps), "d"(a1), "d"(a2) : "memory");
+                        asm volatile("st.global.v2.f64 [%0], {%1, %2};" ::"l"(ps + 2), "d"(a3), "d"(a4) : "memory");
                     }
                 }
                 if constexpr (SRC == 0) {
                     p.state_out[sid] = S & GZ_MASK48;
                 } else {
-                    p.state_out[2 * sid] = S;
-                    p.state_out[2 * sid + 1] = gam;
+                    asm volatile("st.global.v2.u64 [%0], {%1, %2};" ::"l"(p.state_out + 2 * sid), "l"(S), "l"(gam) : "memory");
                 }
             }
             ++k;
             failed = false;
-            ck = 0;
-            a1 = a2 = a3 = a4 = 0.0;
+            if constexpr (STATS) {
+                ck = 0;
+                a1 = a2 = a3 = a4 = 0.0;
+            }
             /* rows start on a chunk boundary */
-            C = (C + 3u) & ~3u;
+            if (n_per & 3) C = (C + 3u) & ~3u;
             f = C;
             c_row0 = C;
-            if (k < ng) {
-                sid = (g0 + (int64_t)k * gstride) * 32 + lane;
-                valid = sid < n_streams;
-                S = S_next;
-                gam = gam_next;
-                load_state(k + 1, S_next, gam_next);
-                rowp = p.out + sid * p.ld;
-                c_rowend = valid ? C + (uint32_t)n_per : C;   /* no stream: skip the row */
-            } else {
-                valid = false;
-                c_rowend = C;
-            }
+            sid += sstride;
+            rowp = rowp_next;
+            rowp_next += rstride;
+            valid = k < ng && sid < n_streams;
+            S = S_next;
+            gam = gam_next;
+            load_state(sid + sstride, S_next, gam_next);
+            c_rowend = valid ? C + (uint32_t)n_per : C;   /* no stream: skip the row */
         }
     };
-    load_state(0, S_next, gam_next);
+    if (ng > 0) load_state(sid + sstride, S_next, gam_next);
     next_row();
 
     while (__any_sync(GZ_FULL, k < ng)) {
@@ -221,7 +228,9 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ 
         {
             const uint32_t n_live = (C - C0) + (frozen ? 1u : 0u);
             GZ_CHECK(n_live <= (uint32_t)TMA_K, n_live);
-            if constexpr (SRC == 0) {
+            if constexpr (SRC == 0 && (LST_EXP & 4)) {
+                S = tcs[CH - 1].state();   /* timing experiment: no jump (wrong results) */
+            } else if constexpr (SRC == 0) {
                 uint64_t ja, jc;
                 lds_tab(jump_sh + 16 * n_live, ja, jc);
                 S = S * ja + jc;
@@ -230,9 +239,6 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ 
             }
         }
         /* ---- the frozen lanes' slow attempts, resolved together ---- */
-#ifndef LST_EXP
-#define LST_EXP 0
-#endif
         /* LST_EXP (timing experiments only, wrong results): 1 no frozen pass, 2 no row stores, 3 neither */
         if ((LST_EXP & 1) == 0 && __any_sync(GZ_FULL, frozen)) {
             if (frozen) {
