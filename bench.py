@@ -14,7 +14,7 @@ step).  The output (8 GiB per GPU per step) is far larger than L2, so no flush
 is needed between steps.
 
 value    = variates/s over all ranks (device time, CUDA events on the launching
-           stream, max over ranks); one kernel (k_zig_tma) per step.
+           stream, max over ranks); one kernel (k_zig_lst) per step.
 e2e      = the same work through the reference-facing host-buffer C-ABI call
            (gz_fill_gaussians_host): stream states in from pinned host memory,
            deviates, states and checksums back to pinned host memory, every step.
@@ -526,7 +526,7 @@ def main():
                        "parallelism": f"streams sharded over {world} GPU(s), no collective on the generation path"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak, "traffic": None if tr is None else tr["bytes_per_launch"],
-                         "peak_kind": peak_kind, "kernel": "k_zig_tma (one launch per step)",
+                         "peak_kind": peak_kind, "kernel": "k_zig_lst (one launch per step)",
                          "algorithmic_bytes_per_launch": kernel_bytes,
                          "traffic_source": None if tr is None else tr.get("source"),
                          "compute_bounds": cb},
