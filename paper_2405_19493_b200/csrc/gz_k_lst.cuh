@@ -34,7 +34,8 @@
  */
 #pragma once
 
-constexpr int LST_SLOTS = 16;   /* staging slots per lane (8 bytes each) */
+/* staging slots per lane (8 bytes each): a round writes TMA_K of them past <= 3 unstored */
+__host__ __device__ constexpr int lst_slots(int k) { return k <= 12 ? 16 : 32; }
 #ifndef LST_EXP
 #define LST_EXP 0
 #endif
@@ -63,7 +64,9 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ 
     constexpr int NL = MOD ? 256 : 128;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     const uint32_t base_sh = sh_addr(smem_raw);
-    constexpr uint32_t RING = NW * 32 * LST_SLOTS * 8;
+    constexpr int SL = lst_slots(TMA_K);
+    constexpr uint32_t SMASK = (SL - 1) << 3;   /* slot bits of a byte offset */
+    constexpr uint32_t RING = NW * 32 * SL * 8;
     ulonglong2* s_kw = reinterpret_cast<ulonglong2*>(smem_raw + RING);
     float2* s_yf = reinterpret_cast<float2*>(smem_raw + RING + NL * 16 * TMA_REP);
     ulonglong2* s_jump = reinterpret_cast<ulonglong2*>(smem_raw + RING + NL * 16 * TMA_REP + NL * 8);
@@ -77,7 +80,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ 
     const int wib = threadIdx.x >> 5;
     const uint32_t lx = (uint32_t)(lane & 7) << 4;
     /* the lane's ring: 128-byte aligned, so slot s is at ((8 s) & 0x78) ^ rowx */
-    const uint32_t rowx = (base_sh + (uint32_t)threadIdx.x * (LST_SLOTS * 8)) ^ lx;
+    const uint32_t rowx = (base_sh + (uint32_t)threadIdx.x * (SL * 8)) ^ lx;
     const uint32_t my_kw = base_sh + RING + lx;   /* replica lane & 7 of the layer rows */
     const uint32_t yf_sh = sh_addr(s_yf);
     const uint32_t jump_sh = sh_addr(s_jump);
@@ -138,7 +141,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ 
                     /* the row's last partial chunk */
                     for (; f < c_rowend; ++f) {
                         uint64_t v;
-                        asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(((f << 3) & 0x78u) ^ rowx));
+                        asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(((f << 3) & SMASK) ^ rowx));
                         rowp[f - c_row0] = __longlong_as_double((long long)v);
                         if constexpr (STATS) tma_fold(v, ck, a1, a2, a3, a4);
                     }
@@ -212,7 +215,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ 
         if (act) {
 #pragma unroll
             for (int kk2 = 0; kk2 < TMA_K; ++kk2) {
-                const uint32_t a = (((C0 + (uint32_t)kk2) << 3) & 0x78u) ^ rowx;
+                const uint32_t a = (((C0 + (uint32_t)kk2) << 3) & SMASK) ^ rowx;
                 asm volatile("st.shared.u64 [%0], %1;" ::"r"(a), "l"(zbs[kk2]) : "memory");
             }
         }
@@ -271,7 +274,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ 
                     ok = to.k >= 0;
                     if (ok) {
                         const uint64_t zb = (uint64_t)__double_as_longlong(x) ^ sgn;
-                        asm volatile("st.shared.u64 [%0], %1;" ::"r"(((C << 3) & 0x78u) ^ rowx), "l"(zb) : "memory");
+                        asm volatile("st.shared.u64 [%0], %1;" ::"r"(((C << 3) & SMASK) ^ rowx), "l"(zb) : "memory");
                     } else {
                         failed = true;
                         gz_raise(GZ_ERR_GUARD, sid);
@@ -285,7 +288,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ 
         /* ---- complete 4-deviate chunks to the row: one 32-byte store each ---- */
         if (!failed) {
             while (C - f >= 4u) {
-                const uint32_t a = ((f << 3) & 0x78u) ^ rowx;   /* slots f .. f+3: two 16-byte chunks */
+                const uint32_t a = ((f << 3) & SMASK) ^ rowx;   /* slots f .. f+3: two 16-byte chunks */
                 uint64_t v0, v1, v2, v3;
                 lds_u64x2_v(a, v0, v1);
                 lds_u64x2_v(a ^ 0x10u, v2, v3);
