@@ -286,25 +286,26 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ 
             }
         }
         /* ---- complete 4-deviate chunks to the row: one 32-byte store each ---- */
-        if (!failed) {
-            while (C - f >= 4u) {
-                const uint32_t a = ((f << 3) & SMASK) ^ rowx;   /* slots f .. f+3: two 16-byte chunks */
-                uint64_t v0, v1, v2, v3;
-                lds_u64x2_v(a, v0, v1);
-                lds_u64x2_v(a ^ 0x10u, v2, v3);
-                double* dst = rowp + (f - c_row0);
-                if ((LST_EXP & 2) == 0 || (v0 ^ v1 ^ v2 ^ v3) == 0x123456789ULL)
-                    asm volatile("st.global.v4.b64 [%0], {%1, %2, %3, %4};" ::"l"(dst), "l"(v0), "l"(v1), "l"(v2), "l"(v3)
-                                 : "memory");
-                if constexpr (STATS) {
-                    ck ^= v0 ^ v1 ^ v2 ^ v3;
-                    tma_fold_fp(v0, a1, a2, a3, a4);
-                    tma_fold_fp(v1, a1, a2, a3, a4);
-                    tma_fold_fp(v2, a1, a2, a3, a4);
-                    tma_fold_fp(v3, a1, a2, a3, a4);
-                }
-                f += 4u;
+        auto store_chunk = [&]() {
+            const uint32_t a = ((f << 3) & SMASK) ^ rowx;   /* slots f .. f+3: two 16-byte chunks */
+            uint64_t v0, v1, v2, v3;
+            lds_u64x2_v(a, v0, v1);
+            lds_u64x2_v(a ^ 0x10u, v2, v3);
+            double* dst = rowp + (f - c_row0);
+            if ((LST_EXP & 2) == 0 || (v0 ^ v1 ^ v2 ^ v3) == 0x123456789ULL)
+                asm volatile("st.global.v4.b64 [%0], {%1, %2, %3, %4};" ::"l"(dst), "l"(v0), "l"(v1), "l"(v2), "l"(v3)
+                             : "memory");
+            if constexpr (STATS) {
+                ck ^= v0 ^ v1 ^ v2 ^ v3;
+                tma_fold_fp(v0, a1, a2, a3, a4);
+                tma_fold_fp(v1, a1, a2, a3, a4);
+                tma_fold_fp(v2, a1, a2, a3, a4);
+                tma_fold_fp(v3, a1, a2, a3, a4);
             }
+            f += 4u;
+        };
+        if (!failed) {
+            while (C - f >= 4u) store_chunk();
         }
         if (C >= c_rowend) next_row();
     }
