@@ -5,26 +5,35 @@
  * rows and a row stride that is a multiple of 4 deviates).
  *
  * Not a standalone header: included by gz_engine.cu inside its anonymous
- * namespace, after gz_k_tma.cuh (whose draw, split, recover and fold helpers
- * it uses).
+ * namespace, after gz_k_tma.cuh (whose recover and fold helpers it uses).
  *
  * A lane owns one stream at a time and steps it exactly as the reference's
  * per-stream loop (engine.py:75-112 original, 114-151 modified ziggurat; the
  * attempt is ZigguratSampler._draw, samplers.py:95-115 / 144-165).  Rounds of
- * TMA_K attempts run without branches, as in k_zig_tma: every attempt's
- * deviate is written to the lane's next staging slot unconditionally, the
- * committed attempts are the leading fast accepts, and the first attempt that
- * is not a fast accept freezes the lane for the rest of the round; the frozen
- * lanes of a warp then resolve their wedge / tail attempts together (one pass
- * per round: recover the draw from the state, draw the wedge's uniform, float
- * pre-filter and the exact glibc exp near the boundary, or the tail loop).
+ * K attempts run without branches: every attempt's deviate is staged
+ * unconditionally, the committed attempts are the leading fast accepts, and
+ * the first attempt that is not a fast accept freezes the lane for the rest of
+ * the round; the frozen lanes of a warp then resolve their wedge / tail
+ * attempts together (one pass per round: the staged x, the recovered layer,
+ * the wedge's uniform, float pre-filter and the exact glibc exp near the
+ * boundary, or the tail loop).
  *
- * Output: each lane stages its row in a private 16-slot ring in shared memory
- * (128 bytes, the 16-byte chunks XOR-swizzled by lane & 7) and, after every
- * round, writes each complete 4-deviate chunk to its row with one 32-byte
- * store (STG.E.256: a full L2 sector).  Lanes never wait for each other: no
- * warp-wide flush, no ring-room stalls, so there is no cross-lane drift, and a
- * warp needs 4 KiB of shared memory instead of 16 KiB -- 20 warps per SM.
+ * Shared memory, laid out for the bank structure (all addresses are 32-bit
+ * shared-window offsets computed once):
+ *  - layer rows: a 64 KiB-aligned table of 256 entries x 256 bytes, entry e =
+ *    layer e mod n (the original ziggurat indexes it with the draw's top byte,
+ *    sign included: entries e and e + 128 hold the same layer), 8 replicas of
+ *    the 16-byte row {ktab, bits(wtab)} per entry, lane & 7 reading its own.
+ *    The gather address is ONE byte permute: the draw's index byte dropped into
+ *    byte 1 of (table base | replica offset).
+ *  - staging: per warp 16 slots x 32 lanes x 8 bytes, slot-major (slot s of lane
+ *    l at s * 256 + l * 8), so every lane owns one bank pair and the per-slot
+ *    stores and chunk loads of a half-warp never conflict whatever the lanes'
+ *    positions.  A lane's unstored deviates always start at slot 0: a round
+ *    writes its K candidates at slots L .. L + K - 1 (L <= 3 unstored), complete
+ *    4-deviate chunks leave from slots 0, 4, 8 with one 32-byte store each
+ *    (STG.E.256: a full L2 sector), and the <= 3 left over move back to slot 0.
+ *    Lanes never wait for each other: no warp-wide flush, no cross-lane drift.
  * Rows of a lane follow each other (lane l of warp g takes the streams
  * (g + k * warps) * 32 + l); the next row's state is loaded when a row starts.
  *
@@ -34,103 +43,115 @@
  */
 #pragma once
 
-/* staging slots per lane (8 bytes each): a round writes TMA_K of them past <= 3 unstored */
-__host__ __device__ constexpr int lst_slots(int k) { return k <= 12 ? 16 : 32; }
-#ifndef LST_EXP
-#define LST_EXP 0
-#endif
-#ifndef LST_CVT
-#define LST_CVT 0
-#endif
+constexpr int LST_SLOTS = 16;                       /* staging slots per lane */
+constexpr uint32_t LST_RING = LST_SLOTS * 256;      /* staging bytes per warp */
+constexpr uint32_t LST_TAB = 0x10000;               /* the layer-row table (64 KiB) */
+/* dynamic shared memory of k_zig_lst for NW warps, n layers and K attempts per round,
+   given the dynamic window's offset (0x400 on sm_100 without clusters; the kernel
+   re-derives the layout from the real base and fails loudly if it does not fit) */
+__host__ __device__ constexpr uint32_t lst_smem_bytes(int NW, int NL, int K, uint32_t base = 0x400)
+{
+    const uint32_t tab = (base + 0xFFFFu) & ~0xFFFFu;
+    const uint32_t na = (tab - base) / LST_RING < (uint32_t)NW ? (tab - base) / LST_RING : (uint32_t)NW;
+    return tab + LST_TAB + ((uint32_t)NW - na) * LST_RING + (uint32_t)NL * 8 + 16u * (uint32_t)(K + 1) - base;
+}
 
-/* (double)m for m = mhi * 2^32 + mlo < 2^56, rounded to nearest even: the classic
-   two-constant conversion -- (2^84 + mhi 2^32) - (2^84 + 2^52) is exact, and the
-   final add of 2^52 + mlo rounds once -- so it equals __ull2double_rn(m) with two
-   fixed-latency DADDs instead of the variable-latency I2F.F64.U64 */
+__device__ __forceinline__ uint64_t lds_u64(uint32_t a)
+{
+    uint64_t v;
+    asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts_u64(uint32_t a, uint64_t v)
+{
+    asm volatile("st.shared.u64 [%0], %1;" ::"r"(a), "l"(v) : "memory");
+}
+
+/* (double)m for m = mhi * 2^32 + mlo < 2^56, rounded to nearest even */
 __device__ __forceinline__ double lst_u56_to_f64(uint32_t mhi, uint32_t mlo)
 {
-    if constexpr (LST_CVT) {
-        const double h = __hiloint2double(0x45300000, (int)mhi);
-        const double l = __hiloint2double(0x43300000, (int)mlo);
-        return __dadd_rn(__dsub_rn(h, 19342813118337666422669312.0 /* 2^84 + 2^52 */), l);
-    } else {
-        return __ull2double_rn(((uint64_t)mhi << 32) | mlo);
-    }
+    return __ull2double_rn(((uint64_t)mhi << 32) | mlo);
 }
 
 template <int SRC, bool MOD, bool STATS, int NW, int TMA_K>
 __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ LaneParams p)
 {
+    static_assert(TMA_K + 3 <= LST_SLOTS, "a round's candidates and the unstored deviates share the staging slots");
     constexpr int NL = MOD ? 256 : 128;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    const uint32_t base_sh = sh_addr(smem_raw);
-    constexpr int SL = lst_slots(TMA_K);
-    constexpr uint32_t SMASK = (SL - 1) << 3;   /* slot bits of a byte offset */
-    constexpr uint32_t RING = NW * 32 * SL * 8;
-    ulonglong2* s_kw = reinterpret_cast<ulonglong2*>(smem_raw + RING);
-    float2* s_yf = reinterpret_cast<float2*>(smem_raw + RING + NL * 16 * TMA_REP);
-    ulonglong2* s_jump = reinterpret_cast<ulonglong2*>(smem_raw + RING + NL * 16 * TMA_REP + NL * 8);
-    for (int j = threadIdx.x; j < NL * TMA_REP; j += blockDim.x) s_kw[j] = p.kw[j / TMA_REP];
-    for (int j = threadIdx.x; j < NL; j += blockDim.x) s_yf[j] = p.yf[j];
-    /* LCG: (A, C) of 2n steps, n <= TMA_K (the state after n draws from a round's start) */
-    if (SRC == 0 && threadIdx.x <= TMA_K) s_jump[threadIdx.x] = make_ulonglong2(c_lcgA[2 * threadIdx.x], c_lcgC[2 * threadIdx.x]);
+    const uint32_t base = sh_addr(smem_raw);
+    uint32_t dyn;
+    asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+    /* the layout of lst_smem_bytes from the real window offset */
+    const uint32_t tab = (base + 0xFFFFu) & ~0xFFFFu;
+    const uint32_t na = min((uint32_t)NW, (tab - base) / LST_RING);
+    const uint32_t after = tab + LST_TAB;
+    const uint32_t yf_sh = after + ((uint32_t)NW - na) * LST_RING;
+    const uint32_t jump_sh = yf_sh + NL * 8;
+    if (jump_sh + 16u * (TMA_K + 1) > base + dyn) {
+        if (threadIdx.x == 0) gz_raise(GZ_ERR_CHECK, __LINE__);
+        return;
+    }
+    for (int j = threadIdx.x; j < 256 * TMA_REP; j += blockDim.x) {
+        const ulonglong2 v = p.kw[(j / TMA_REP) & (NL - 1)];
+        asm volatile("st.shared.v2.u64 [%0], {%1, %2};" ::"r"(tab + (uint32_t)(j / TMA_REP) * 256 + (uint32_t)(j % TMA_REP) * 16),
+                     "l"(v.x), "l"(v.y)
+                     : "memory");
+    }
+    for (int j = threadIdx.x; j < NL; j += blockDim.x) {
+        const float2 v = p.yf[j];
+        asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(yf_sh + 8 * j), "f"(v.x), "f"(v.y) : "memory");
+    }
+    /* LCG: (A, C) of 2n steps, n <= K (the state after n draws from a round's start) */
+    if (SRC == 0 && threadIdx.x <= TMA_K)
+        asm volatile("st.shared.v2.u64 [%0], {%1, %2};" ::"r"(jump_sh + 16 * threadIdx.x), "l"(c_lcgA[2 * threadIdx.x]),
+                     "l"(c_lcgC[2 * threadIdx.x])
+                     : "memory");
     __syncthreads();
 
     const int lane = threadIdx.x & 31;
-    const int wib = threadIdx.x >> 5;
-    const uint32_t lx = (uint32_t)(lane & 7) << 4;
-    /* the lane's ring: 128-byte aligned, so slot s is at ((8 s) & 0x78) ^ rowx */
-    const uint32_t rowx = (base_sh + (uint32_t)threadIdx.x * (SL * 8)) ^ lx;
-    const uint32_t my_kw = base_sh + RING + lx;   /* replica lane & 7 of the layer rows */
-    const uint32_t yf_sh = sh_addr(s_yf);
-    const uint32_t jump_sh = sh_addr(s_jump);
-    const uint64_t lcg_inc = SRC == 0 ? ld_keep(&c_lcgC[1]) : 0;
-    const uint64_t lcg_inc2 = SRC == 0 ? ld_keep(&c_lcgC[2]) : 0;
-    uint64_t jA[TMA_CHV > 1 ? TMA_CHV : 1], jC[TMA_CHV > 1 ? TMA_CHV : 1];
-#pragma unroll
-    for (int j = 0; j < (TMA_CHV > 1 ? TMA_CHV : 1); ++j) {
-        jA[j] = (SRC == 0 && j > 0) ? ld_keep(&c_lcgA[2 * (TMA_K / TMA_CHV) * j]) : 0;
-        jC[j] = (SRC == 0 && j > 0) ? ld_keep(&c_lcgC[2 * (TMA_K / TMA_CHV) * j]) : 0;
-    }
+    const uint32_t wib = threadIdx.x >> 5;
+    /* the lane's staging column (slot s at ringl + 256 s) and its replica of the layer rows */
+    const uint32_t ringl = (wib < na ? base + wib * LST_RING : after + (wib - na) * LST_RING) + (uint32_t)lane * 8;
+    const uint32_t kwl = tab | ((uint32_t)(lane & 7) << 4);
     const int n_per = p.n_per;
+    /* the increments of one and two LCG steps, C and A C + C, held in registers */
+    const uint64_t inc1 = SRC == 0 ? ld_keep(&c_lcgC[1]) : 0, inc2 = SRC == 0 ? ld_keep(&c_lcgC[2]) : 0;
     const uint32_t guard32 = p.guard > 0xffffffffll ? 0xffffffffu : (uint32_t)p.guard;
-    const int64_t n_streams = p.n_streams;
-    const int64_t n_groups = (n_streams + 31) >> 5;
-    const int64_t gstride = (int64_t)gridDim.x * NW;
-    const int64_t g0 = (int64_t)blockIdx.x * NW + wib;
+    /* stream ids in 32 bits: n_streams < 2^31 (lst_eligible), so id + 2 * sstride < 2^32 */
+    const uint32_t n_streams = (uint32_t)p.n_streams;
+    const uint32_t n_groups = (uint32_t)(((int64_t)p.n_streams + 31) >> 5);
+    const uint32_t gstride = gridDim.x * NW;
+    const uint32_t g0 = blockIdx.x * NW + wib;
     const int ng = g0 < n_groups ? (int)((n_groups - g0 + gstride - 1) / gstride) : 0;
 
     /* the lane's rows: k = 0 .. ng-1, stream (g0 + k gstride) * 32 + lane (if < n_streams) */
     int k = -1;
-    int64_t sid = 0;
     bool valid = false, failed = false;
-    uint64_t S = 0, gam = lcg_inc;
-    uint64_t S_next = 0, gam_next = lcg_inc;   /* the next row's state, loaded a row ahead */
-    uint32_t C = 0;          /* deviates committed by this lane (all rows; slot = C mod 16) */
+    uint64_t S = 0, gam = 0;
+    uint64_t S_next = 0, gam_next = 0;   /* the next row's state, loaded a row ahead */
+    uint32_t C = 0;          /* deviates committed by this lane (all rows) */
     uint32_t c_row0 = 0;     /* C at the start of the current row */
     uint32_t c_rowend = 0;   /* C at its end */
-    uint32_t f = 0;          /* deviates stored */
+    uint32_t f = 0;          /* deviates stored; the unstored ones C - f <= 3 sit at slots 0.. */
     uint32_t rej = 0, c_rej = 0xffffffffu;
-    double* rowp = nullptr;
     uint64_t ck = 0;
     double a1 = 0.0, a2 = 0.0, a3 = 0.0, a4 = 0.0;
 
-    /* consecutive rows of a lane are sstride streams apart: stream, row and state
-       pointers advance by constant strides (no 64-bit multiplies per row) */
-    const int64_t sstride = gstride * 32;
-    const int64_t last = n_streams - 1;
-    sid = g0 * 32 + lane - sstride;
-    double* rowp_next = p.out + (g0 * 32 + lane) * p.ld;
-    const int64_t rstride = sstride * p.ld;
-    /* the next row's state, loaded a row ahead (clamped to a valid stream, so the load is
-       unconditional and lands in its own registers) */
-    auto load_state = [&](int64_t q, uint64_t& s, uint64_t& g) {
-        if (q > last) q = last;
+    /* consecutive rows of a lane are sstride streams apart */
+    const uint32_t sstride = gstride * 32;
+    const uint32_t last = n_streams - 1;
+    uint32_t sid = g0 * 32 + (uint32_t)lane - sstride;   /* modular: the first row adds sstride back */
+    double* rowp = nullptr;
+    double* rowp_next = p.out + (int64_t)(g0 * 32 + (uint32_t)lane) * p.ld;
+    const int64_t rstride = (int64_t)sstride * p.ld;
+    auto load_state = [&](uint32_t q, uint64_t& s, uint64_t& g) {
+        q = min(q, last);   /* clamped: the load is unconditional */
         if constexpr (SRC == 0) {
             s = ld_keep(p.state_in + q);
         } else {
-            s = ld_keep(p.state_in + 2 * q);
-            g = ld_keep(p.state_in + 2 * q + 1);
+            s = ld_keep(p.state_in + 2 * (int64_t)q);
+            g = ld_keep(p.state_in + 2 * (int64_t)q + 1);
         }
     };
     /* the row transition (divergent: once per row and lane): finish the row, start the next */
@@ -138,11 +159,10 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ 
         while (C >= c_rowend && k < ng) {
             if (valid && !failed) {
                 if (n_per & 3) {
-                    /* the row's last partial chunk */
-                    for (; f < c_rowend; ++f) {
-                        uint64_t v;
-                        asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(((f << 3) & SMASK) ^ rowx));
-                        rowp[f - c_row0] = __longlong_as_double((long long)v);
+                    /* the row's last partial chunk (slots 0 .. c_rowend - f - 1) */
+                    for (uint32_t q = 0; q < c_rowend - f; ++q) {
+                        const uint64_t v = lds_u64(ringl + 256 * q);
+                        rowp[f + q - c_row0] = __longlong_as_double((long long)v);
                         if constexpr (STATS) tma_fold(v, ck, a1, a2, a3, a4);
                     }
                 }
@@ -150,7 +170,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ 
                 if constexpr (STATS) {
                     if (p.checksum) p.checksum[sid] = ck;
                     if (p.psum) {
-                        double* ps = p.psum + 4 * sid;   /* 16-byte aligned (lst_eligible) */
+                        double* ps = p.psum + 4 * (int64_t)sid;   /* 16-byte aligned (lst_eligible) */
                         asm volatile("st.global.v2.f64 [%0], {%1, %2};" ::"l"(ps), "d"(a1), "d"(a2) : "memory");
                         asm volatile("st.global.v2.f64 [%0], {%1, %2};" ::"l"(ps + 2), "d"(a3), "d"(a4) : "memory");
                     }
@@ -158,7 +178,8 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ 
                 if constexpr (SRC == 0) {
                     p.state_out[sid] = S & GZ_MASK48;
                 } else {
-                    asm volatile("st.global.v2.u64 [%0], {%1, %2};" ::"l"(p.state_out + 2 * sid), "l"(S), "l"(gam) : "memory");
+                    asm volatile("st.global.v2.u64 [%0], {%1, %2};" ::"l"(p.state_out + 2 * (int64_t)sid), "l"(S), "l"(gam)
+                                 : "memory");
                 }
             }
             ++k;
@@ -167,7 +188,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ 
                 ck = 0;
                 a1 = a2 = a3 = a4 = 0.0;
             }
-            /* rows start on a chunk boundary */
+            /* rows start on a chunk boundary, with nothing unstored */
             if (n_per & 3) C = (C + 3u) & ~3u;
             f = C;
             c_row0 = C;
@@ -188,36 +209,58 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ 
         /* ---- one round: TMA_K attempts per lane, no branches ---- */
         const bool act = C < c_rowend;
         const uint32_t C0 = C;
-        /* LCG: CH independent draw chains (chain j starts 2 KC j steps ahead by one jump) */
-        constexpr int CH = (SRC == 0 && TMA_K % TMA_CHV == 0) ? TMA_CHV : 1, KC = TMA_K / CH;
-        TmaCursor<SRC> tcs[CH] = {TmaCursor<SRC>(S)};
-#pragma unroll
-        for (int j = 1; j < CH; ++j) tcs[j] = TmaCursor<SRC>(S * jA[j] + jC[j]);
         uint32_t fm = 0;
-        /* the deviates are kept in registers and stored after the last attempt: a table
-           gather may not pass a shared store in program order (ptxas cannot tell that
-           they never alias), so storing inside the loop would serialise the attempts */
+        /* the deviates stay in registers until the last attempt: a table gather may not
+           pass a shared store in program order (ptxas cannot tell that they never alias) */
         uint64_t zbs[TMA_K];
+        uint32_t sl = (uint32_t)S, sh = (uint32_t)(S >> 32);
 #pragma unroll
         for (int kk2 = 0; kk2 < TMA_K; ++kk2) {
             uint32_t uhi, ulo;
-            tcs[kk2 / KC].draw(gam, lcg_inc2, uhi, ulo);
-            uint32_t ioff, mhi, mlo, sgn;
-            tma_split32<MOD>(uhi, ulo, ioff, mhi, mlo, sgn);
+            if constexpr (SRC == 0) {
+                /* u64 = two steps, t1 = A t + C and t2 = A^2 t + (A C + C) straight from t
+                   (engine.py:52-58: bits 16..47 of each state) */
+                uint32_t t1l, t1h, t2l, t2h;
+                lcg_step32(sl, sh, t1l, t1h, inc1);
+                const uint64_t p2 = (uint64_t)sl * 0xB4600A69u + inc2;
+                t2l = (uint32_t)p2;
+                t2h = (uint32_t)(p2 >> 32) + sh * 0xB4600A69u + sl * 0xBB20u;
+                uhi = __funnelshift_r(t1l, t1h, 16);
+                ulo = __funnelshift_r(t2l, t2h, 16);
+                sl = t2l;
+                sh = t2h;
+            } else {
+                const uint64_t t = (((uint64_t)sh << 32) | sl) + gam;
+                sl = (uint32_t)t;
+                sh = (uint32_t)(t >> 32);
+                const uint64_t u = gz_mix64(t);
+                uhi = (uint32_t)(u >> 32);
+                ulo = (uint32_t)u;
+            }
+            uint32_t mhi, mlo, sgn, row;
+            if constexpr (MOD) {
+                row = __byte_perm(ulo, kwl, 0x7604);   /* layer = low byte */
+                mlo = __funnelshift_r(ulo, uhi, 9);
+                mhi = uhi >> 9;
+                sgn = (ulo << 23) & 0x80000000u;
+            } else {
+                row = __byte_perm(uhi, kwl, 0x7634);   /* sign and layer = top byte */
+                mhi = uhi & 0x00ffffffu;
+                mlo = ulo;
+                sgn = uhi & 0x80000000u;
+            }
             uint64_t kk, wb;
-            lds_tab(my_kw + ioff, kk, wb);
+            lds_tab(row, kk, wb);
             const uint64_t m = ((uint64_t)mhi << 32) | mlo;
             const double x = __dmul_rn(lst_u56_to_f64(mhi, mlo), __longlong_as_double((long long)wb));
             if (m < kk) fm |= 1u << kk2;
             zbs[kk2] = (uint64_t)__double_as_longlong(x) ^ ((uint64_t)sgn << 32);
-            GZ_CHECK(ioff < NL * 128u, ioff);
         }
+        const uint32_t wbase = ringl + (C0 - f) * 256;   /* slot of deviate C0 */
         if (act) {
 #pragma unroll
-            for (int kk2 = 0; kk2 < TMA_K; ++kk2) {
-                const uint32_t a = (((C0 + (uint32_t)kk2) << 3) & SMASK) ^ rowx;
-                asm volatile("st.shared.u64 [%0], %1;" ::"r"(a), "l"(zbs[kk2]) : "memory");
-            }
+            for (int kk2 = 0; kk2 < TMA_K; ++kk2)
+                asm volatile("st.shared.u64 [%0], %1;" ::"r"(wbase + 256 * kk2), "l"(zbs[kk2]) : "memory");
         }
         bool frozen = false;
         if (act) {
@@ -231,9 +274,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ 
         {
             const uint32_t n_live = (C - C0) + (frozen ? 1u : 0u);
             GZ_CHECK(n_live <= (uint32_t)TMA_K, n_live);
-            if constexpr (SRC == 0 && (LST_EXP & 4)) {
-                S = tcs[CH - 1].state();   /* timing experiment: no jump (wrong results) */
-            } else if constexpr (SRC == 0) {
+            if constexpr (SRC == 0) {
                 uint64_t ja, jc;
                 lds_tab(jump_sh + 16 * n_live, ja, jc);
                 S = S * ja + jc;
@@ -242,20 +283,18 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ 
             }
         }
         /* ---- the frozen lanes' slow attempts, resolved together ---- */
-        /* LST_EXP (timing experiments only, wrong results): 1 no frozen pass, 2 no row stores, 3 neither */
-        if ((LST_EXP & 1) == 0 && __any_sync(GZ_FULL, frozen)) {
+        if (__any_sync(GZ_FULL, frozen)) {
             if (frozen) {
+                const uint32_t slot = ringl + (C - f) * 256;   /* the frozen attempt's staged x */
                 const uint64_t u = tma_recover<SRC>(S);
                 uint32_t i;
-                uint64_t m, sgn;
-                tma_split<MOD>(u, i, m, sgn);
-                uint64_t kk, wb;
-                lds_tab(my_kw + (i << 7), kk, wb);
-                double x = __dmul_rn(__ull2double_rn(m), __longlong_as_double((long long)wb));
+                uint64_t m_unused, sgn;
+                tma_split<MOD>(u, i, m_unused, sgn);
+                double x = __longlong_as_double((long long)(lds_u64(slot) & 0x7fffffffffffffffULL));
                 bool ok;
                 if (i != 0) {
                     /* wedge: the next draw is its uniform, whatever the outcome; an accepted
-                       wedge's slot already holds x (written in the round) */
+                       wedge's slot already holds x */
                     const uint64_t u2 = tma_draw<SRC>(S, gam);
                     ok = wedge_accept_f(u2, x, p.yd + i, lds_f32x2(yf_sh + 8 * i));
                     if (!ok) {
@@ -274,7 +313,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ 
                     ok = to.k >= 0;
                     if (ok) {
                         const uint64_t zb = (uint64_t)__double_as_longlong(x) ^ sgn;
-                        asm volatile("st.shared.u64 [%0], %1;" ::"r"(((C << 3) & SMASK) ^ rowx), "l"(zb) : "memory");
+                        asm volatile("st.shared.u64 [%0], %1;" ::"r"(slot), "l"(zb) : "memory");
                     } else {
                         failed = true;
                         gz_raise(GZ_ERR_GUARD, sid);
@@ -285,27 +324,33 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ 
                 if (ok) ++C;
             }
         }
-        /* ---- complete 4-deviate chunks to the row: one 32-byte store each ---- */
-        auto store_chunk = [&]() {
-            const uint32_t a = ((f << 3) & SMASK) ^ rowx;   /* slots f .. f+3: two 16-byte chunks */
-            uint64_t v0, v1, v2, v3;
-            lds_u64x2_v(a, v0, v1);
-            lds_u64x2_v(a ^ 0x10u, v2, v3);
+        /* ---- complete 4-deviate chunks to the row: one 32-byte store each, from slots
+           0, 4, 8; the <= 3 left over move back to slot 0 ---- */
+        if (!failed) {
+            uint32_t ph = ringl;
             double* dst = rowp + (f - c_row0);
-            if ((LST_EXP & 2) == 0 || (v0 ^ v1 ^ v2 ^ v3) == 0x123456789ULL)
+#pragma unroll 1
+            while (C - f >= 4u) {
+                const uint64_t v0 = lds_u64(ph), v1 = lds_u64(ph + 256), v2 = lds_u64(ph + 512), v3 = lds_u64(ph + 768);
                 asm volatile("st.global.v4.b64 [%0], {%1, %2, %3, %4};" ::"l"(dst), "l"(v0), "l"(v1), "l"(v2), "l"(v3)
                              : "memory");
-            if constexpr (STATS) {
-                ck ^= v0 ^ v1 ^ v2 ^ v3;
-                tma_fold_fp(v0, a1, a2, a3, a4);
-                tma_fold_fp(v1, a1, a2, a3, a4);
-                tma_fold_fp(v2, a1, a2, a3, a4);
-                tma_fold_fp(v3, a1, a2, a3, a4);
+                if constexpr (STATS) {
+                    ck ^= v0 ^ v1 ^ v2 ^ v3;
+                    tma_fold_fp(v0, a1, a2, a3, a4);
+                    tma_fold_fp(v1, a1, a2, a3, a4);
+                    tma_fold_fp(v2, a1, a2, a3, a4);
+                    tma_fold_fp(v3, a1, a2, a3, a4);
+                }
+                f += 4u;
+                ph += 1024u;
+                dst += 4;
             }
-            f += 4u;
-        };
-        if (!failed) {
-            while (C - f >= 4u) store_chunk();
+            if (ph != ringl) {
+                const uint64_t w0 = lds_u64(ph), w1 = lds_u64(ph + 256), w2 = lds_u64(ph + 512);
+                sts_u64(ringl, w0);
+                sts_u64(ringl + 256, w1);
+                sts_u64(ringl + 512, w2);
+            }
         }
         if (C >= c_rowend) next_row();
     }
