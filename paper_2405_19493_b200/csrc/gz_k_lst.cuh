@@ -142,9 +142,8 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ 
     const uint32_t sstride = gstride * 32;
     const uint32_t last = n_streams - 1;
     uint32_t sid = g0 * 32 + (uint32_t)lane - sstride;   /* modular: the first row adds sstride back */
-    double* rowp = nullptr;
-    double* rowp_next = p.out + (int64_t)(g0 * 32 + (uint32_t)lane) * p.ld;
     const int64_t rstride = (int64_t)sstride * p.ld;
+    double* rowp = p.out + (int64_t)(g0 * 32 + (uint32_t)lane) * p.ld - rstride;
     auto load_state = [&](uint32_t q, uint64_t& s, uint64_t& g) {
         q = min(q, last);   /* clamped: the load is unconditional */
         if constexpr (SRC == 0) {
@@ -154,9 +153,10 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ 
             g = ld_keep(p.state_in + 2 * (int64_t)q + 1);
         }
     };
-    /* the row transition (divergent: once per row and lane): finish the row, start the next */
+    /* the row transition (divergent: once per row and lane, called when C >= c_rowend and
+       k < ng): finish the row, start the next (at most one per round) */
     auto next_row = [&]() {
-        while (C >= c_rowend && k < ng) {
+        {
             if (valid && !failed) {
                 if (n_per & 3) {
                     /* the row's last partial chunk (slots 0 .. c_rowend - f - 1) */
@@ -193,8 +193,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ 
             f = C;
             c_row0 = C;
             sid += sstride;
-            rowp = rowp_next;
-            rowp_next += rstride;
+            rowp += rstride;
             valid = k < ng && sid < n_streams;
             S = S_next;
             gam = gam_next;
@@ -325,33 +324,39 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ 
             }
         }
         /* ---- complete 4-deviate chunks to the row: one 32-byte store each, from slots
-           0, 4, 8; the <= 3 left over move back to slot 0 ---- */
+           0, 4, 8 (straight-line, at most (K + 3) / 4 of them); the <= 3 left over move
+           back to slot 0 ---- */
         if (!failed) {
-            uint32_t ph = ringl;
+            const uint32_t pend = C - f;   /* <= K + 3 */
             double* dst = rowp + (f - c_row0);
-#pragma unroll 1
-            while (C - f >= 4u) {
-                const uint64_t v0 = lds_u64(ph), v1 = lds_u64(ph + 256), v2 = lds_u64(ph + 512), v3 = lds_u64(ph + 768);
-                asm volatile("st.global.v4.b64 [%0], {%1, %2, %3, %4};" ::"l"(dst), "l"(v0), "l"(v1), "l"(v2), "l"(v3)
-                             : "memory");
-                if constexpr (STATS) {
-                    ck ^= v0 ^ v1 ^ v2 ^ v3;
-                    tma_fold_fp(v0, a1, a2, a3, a4);
-                    tma_fold_fp(v1, a1, a2, a3, a4);
-                    tma_fold_fp(v2, a1, a2, a3, a4);
-                    tma_fold_fp(v3, a1, a2, a3, a4);
+            uint32_t nst = 0;
+#pragma unroll
+            for (int q = 0; q < (TMA_K + 3) / 4; ++q) {
+                if (pend >= 4u * (q + 1)) {
+                    const uint32_t ph = ringl + 1024u * q;
+                    const uint64_t v0 = lds_u64(ph), v1 = lds_u64(ph + 256), v2 = lds_u64(ph + 512), v3 = lds_u64(ph + 768);
+                    asm volatile("st.global.v4.b64 [%0], {%1, %2, %3, %4};" ::"l"(dst + 4 * q), "l"(v0), "l"(v1), "l"(v2),
+                                 "l"(v3)
+                                 : "memory");
+                    if constexpr (STATS) {
+                        ck ^= v0 ^ v1 ^ v2 ^ v3;
+                        tma_fold_fp(v0, a1, a2, a3, a4);
+                        tma_fold_fp(v1, a1, a2, a3, a4);
+                        tma_fold_fp(v2, a1, a2, a3, a4);
+                        tma_fold_fp(v3, a1, a2, a3, a4);
+                    }
+                    nst = q + 1;
                 }
-                f += 4u;
-                ph += 1024u;
-                dst += 4;
             }
-            if (ph != ringl) {
+            if (nst != 0) {
+                const uint32_t ph = ringl + 1024u * nst;
                 const uint64_t w0 = lds_u64(ph), w1 = lds_u64(ph + 256), w2 = lds_u64(ph + 512);
                 sts_u64(ringl, w0);
                 sts_u64(ringl + 256, w1);
                 sts_u64(ringl + 512, w2);
+                f += 4u * nst;
             }
         }
-        if (C >= c_rowend) next_row();
+        if (C >= c_rowend && k < ng) next_row();
     }
 }
