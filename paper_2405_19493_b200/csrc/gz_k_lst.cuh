@@ -40,6 +40,17 @@
  * Fused witnesses (STATS): the per-row xor checksum (bench.py:174-175) and
  * power sums (stats.py:232-259) are folded from each stored chunk in deviate
  * order -- the order of k_zig_tma and of the oracle's default digest.
+ *
+ * EPI_MUTATE (config 5, x += sigma * z over every gene of `generations`
+ * generations, samplers.py:195-200 with mu = x): a lane's row is one individual,
+ * generations x n_genes deviates long; a chunk of 4 deviates updates 4 genes
+ * (x + sigma z, two roundings) with one 32-byte load and one 32-byte store.  Every
+ * round loads the x of the next two chunks into the same registers (the next round
+ * stores at most two; a register shift of in-flight loads would wait for them) and
+ * prefetches the LST_XPF chunks after them into L1; generation g + 1
+ * reads genes that generation g stored n_genes deviates earlier, in the same thread.
+ * Warps take their groups round-robin over the blocks (g = block + warp * blocks),
+ * so a launch with fewer groups than warp slots still spreads over every SM.
  */
 #pragma once
 
@@ -67,16 +78,35 @@ __device__ __forceinline__ void sts_u64(uint32_t a, uint64_t v)
     asm volatile("st.shared.u64 [%0], %1;" ::"r"(a), "l"(v) : "memory");
 }
 
+#ifndef LST_XPF
+#define LST_XPF 4   /* EPI_MUTATE: prefetch window beyond the two loaded x chunks (L1; 2: 244, 4: 248, 6: 247.5 G/s on c5) */
+#endif
+#ifndef LST_XPF_L2
+#define LST_XPF_L2 0
+#endif
+/* EPI_MUTATE helpers: four genes in with one 32-byte load, x + sigma z */
+__device__ __forceinline__ void ldg_x4(const double* a, uint64_t (&v)[4])
+{
+    asm volatile("ld.global.v4.b64 {%0, %1, %2, %3}, [%4];" : "=l"(v[0]), "=l"(v[1]), "=l"(v[2]), "=l"(v[3]) : "l"(a));
+}
+__device__ __forceinline__ uint64_t mut_x(uint64_t x, double sig, uint64_t zb)
+{
+    return (uint64_t)__double_as_longlong(
+        __dadd_rn(__longlong_as_double((long long)x), __dmul_rn(sig, __longlong_as_double((long long)zb))));
+}
+
 /* (double)m for m = mhi * 2^32 + mlo < 2^56, rounded to nearest even */
 __device__ __forceinline__ double lst_u56_to_f64(uint32_t mhi, uint32_t mlo)
 {
     return __ull2double_rn(((uint64_t)mhi << 32) | mlo);
 }
 
-template <int SRC, bool MOD, bool STATS, int NW, int TMA_K>
+template <int SRC, bool MOD, bool STATS, int NW, int TMA_K, int EPI = EPI_STORE>
 __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ LaneParams p)
 {
     static_assert(TMA_K + 3 <= LST_SLOTS, "a round's candidates and the unstored deviates share the staging slots");
+    constexpr bool MUT = EPI == EPI_MUTATE;
+    static_assert(!MUT || (!STATS && TMA_K <= 8), "the mutation keeps the x of two chunks in registers");
     constexpr int NL = MOD ? 256 : 128;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     const uint32_t base = sh_addr(smem_raw);
@@ -122,7 +152,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ 
     const uint32_t n_streams = (uint32_t)p.n_streams;
     const uint32_t n_groups = (uint32_t)(((int64_t)p.n_streams + 31) >> 5);
     const uint32_t gstride = gridDim.x * NW;
-    const uint32_t g0 = blockIdx.x * NW + wib;
+    const uint32_t g0 = blockIdx.x + wib * gridDim.x;   /* round-robin over the blocks */
     const int ng = g0 < n_groups ? (int)((n_groups - g0 + gstride - 1) / gstride) : 0;
 
     /* the lane's rows: k = 0 .. ng-1, stream (g0 + k gstride) * 32 + lane (if < n_streams) */
@@ -137,6 +167,12 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ 
     uint32_t rej = 0, c_rej = 0xffffffffu;
     uint64_t ck = 0;
     double a1 = 0.0, a2 = 0.0, a3 = 0.0, a4 = 0.0;
+    /* EPI_MUTATE: the row length, the gene of deviate f, the row's sigma and the x of the
+       chunks at genes gpos and gpos + 4 (loaded a round ahead) */
+    const uint32_t rowlen = MUT ? (uint32_t)n_per * (uint32_t)p.generations : (uint32_t)n_per;
+    uint32_t gpos = 0;
+    double sig = 0.0;
+    uint64_t xa[2][4] = {};
 
     /* consecutive rows of a lane are sstride streams apart */
     const uint32_t sstride = gstride * 32;
@@ -198,7 +234,15 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ 
             S = S_next;
             gam = gam_next;
             load_state(sid + sstride, S_next, gam_next);
-            c_rowend = valid ? C + (uint32_t)n_per : C;   /* no stream: skip the row */
+            c_rowend = valid ? C + rowlen : C;   /* no stream: skip the row */
+            if constexpr (MUT) {
+                if (valid) {
+                    gpos = 0;
+                    sig = p.sigma[sid];
+                    ldg_x4(rowp, xa[0]);
+                    ldg_x4(rowp + 4, xa[1]);
+                }
+            }
         }
     };
     if (ng > 0) load_state(sid + sstride, S_next, gam_next);
@@ -328,13 +372,22 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ 
            back to slot 0 ---- */
         if (!failed) {
             const uint32_t pend = C - f;   /* <= K + 3 */
-            double* dst = rowp + (f - c_row0);
+            double* dst = rowp + (MUT ? gpos : f - c_row0);
             uint32_t nst = 0;
 #pragma unroll
             for (int q = 0; q < (TMA_K + 3) / 4; ++q) {
                 if (pend >= 4u * (q + 1)) {
                     const uint32_t ph = ringl + 1024u * q;
-                    const uint64_t v0 = lds_u64(ph), v1 = lds_u64(ph + 256), v2 = lds_u64(ph + 512), v3 = lds_u64(ph + 768);
+                    uint64_t v0 = lds_u64(ph), v1 = lds_u64(ph + 256), v2 = lds_u64(ph + 512), v3 = lds_u64(ph + 768);
+                    if constexpr (MUT) {
+                        /* x + sigma z (gaussian_affine with mu = x: two roundings) */
+                        v0 = mut_x(xa[q][0], sig, v0);
+                        v1 = mut_x(xa[q][1], sig, v1);
+                        v2 = mut_x(xa[q][2], sig, v2);
+                        v3 = mut_x(xa[q][3], sig, v3);
+                        /* genes gpos + 4 q .. + 3 of the row; gpos + 4 wraps to gene 0 */
+                        if (q == 1 && gpos + 4u == (uint32_t)n_per) dst -= n_per;
+                    }
                     asm volatile("st.global.v4.b64 [%0], {%1, %2, %3, %4};" ::"l"(dst + 4 * q), "l"(v0), "l"(v1), "l"(v2),
                                  "l"(v3)
                                  : "memory");
@@ -355,6 +408,31 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ 
                 sts_u64(ringl + 256, w1);
                 sts_u64(ringl + 512, w2);
                 f += 4u * nst;
+                if constexpr (MUT) {
+                    gpos += 4u * nst;
+                    if (gpos >= (uint32_t)n_per) gpos -= (uint32_t)n_per;
+                }
+            }
+            if constexpr (MUT) {
+                /* the x of the next two chunks, a round ahead, always into the same registers
+                   (a conditional shift of the in-flight registers would make the compiler copy
+                   them and wait for the loads); past the row's end they reread this row */
+                if (valid) {
+                    uint32_t g1 = gpos + 4u;
+                    if (g1 == (uint32_t)n_per) g1 = 0;
+                    ldg_x4(rowp + gpos, xa[0]);
+                    ldg_x4(rowp + g1, xa[1]);
+                    /* the chunks that entered the prefetch window [gpos, gpos + 4 (2 + XPF)) */
+#pragma unroll
+                    for (int j = 0; j < 2; ++j) {
+                        if ((uint32_t)j < nst) {
+                            uint32_t g = gpos + 4u * (2 + LST_XPF - nst + j);
+                            if (g >= (uint32_t)n_per) g -= (uint32_t)n_per;
+                            if (LST_XPF_L2) asm volatile("prefetch.global.L2 [%0];" ::"l"(rowp + g));
+                            else asm volatile("prefetch.global.L1 [%0];" ::"l"(rowp + g));
+                        }
+                    }
+                }
             }
         }
         if (C >= c_rowend && k < ng) next_row();
