@@ -32,8 +32,8 @@ if [ "$PART" = 1 ]; then
   summ c4_k_zig_lst
 else
   cap c3_k_zig_lst k_zig_lst c3
-  cap c2_k_polar_q k_polar_q c2
-  cap c5_k_zig_tma_mutate k_zig_tma c5
+  cap c2_k_polar_lst k_polar_lst c2
+  cap c5_k_zig_lst_mutate k_zig_lst c5
   cap c1_k_zig_lseg k_zig_lseg c1
 fi
 ls -la $O
