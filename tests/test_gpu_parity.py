@@ -212,6 +212,36 @@ def test_strided_rows_and_fused_witnesses(policy):
     np.testing.assert_allclose(ps.cpu().numpy(), ps_ref, rtol=1e-12, atol=1e-9)
 
 
+@pytest.mark.parametrize("n,n_per,ld", [(40000, 255, 256), (33000, 17, 20), (2011, 101, 104), (700, 3, 4)])
+def test_polar_lane_odd_rows_strided_with_spares(n, n_per, ld):
+    """k_polar_lst (polar, a lane per stream; the auto choice from 32768 streams, policy
+    'lane' below) on odd row lengths inside 32-byte-aligned strided rows: incoming
+    spares first, the last pair's second deviate carried out as the spare, the padding
+    untouched -- against the oracle, per stream."""
+    rng = np.random.default_rng(n * 1000 + n_per)
+    st_np = O.config_states("c2", range(n))
+    has = rng.integers(0, 2, size=n).astype(np.uint8)
+    spare = rng.standard_normal(n) * has
+    st = dev_states("lcg48", st_np)
+    big = torch.full((n, ld), -9.0, dtype=torch.float64, device=DEV)
+    out = big[:, :n_per]
+    sp = torch.from_numpy(spare).to(DEV)
+    hs = torch.from_numpy(has).to(DEV)
+    if n < 32768:
+        streams.set_kernel_policy("lane")
+    try:
+        streams.fill_gaussians_streams("polar", "lcg48", st, out, spare=sp, has_spare=hs)
+    finally:
+        streams.set_kernel_policy("auto")
+    ref, ref_st, ref_sp, ref_has, status = O.fill_gaussians("polar", "lcg48", st_np, n_per, spare, has)
+    assert status == 0
+    assert bits_equal(out.cpu().numpy(), ref)
+    assert (big[:, n_per:] == -9.0).all()
+    assert np.array_equal(u64(st), ref_st)
+    assert np.array_equal(hs.cpu().numpy(), ref_has)
+    assert bits_equal(sp.cpu().numpy() * (ref_has > 0), ref_sp * (ref_has > 0))
+
+
 # ---- the five configs ---------------------------------------------------------
 
 def test_config1_full(golden):
