@@ -64,7 +64,16 @@ __host__ __device__ constexpr uint32_t lst_smem_bytes(int NW, int NL, int K, uin
 {
     const uint32_t tab = (base + 0xFFFFu) & ~0xFFFFu;
     const uint32_t na = (tab - base) / LST_RING < (uint32_t)NW ? (tab - base) / LST_RING : (uint32_t)NW;
-    return tab + LST_TAB + ((uint32_t)NW - na) * LST_RING + (uint32_t)NL * 8 + 16u * (uint32_t)(K + 1) - base;
+    return tab + LST_TAB + ((uint32_t)NW - na) * LST_RING + (uint32_t)NL * 8 + 16u * (uint32_t)(K + 1) + 16u +
+           (uint32_t)NW * 32u * 16u - base;
+}
+
+/* the next row's state, copied global -> shared without a register (cp.async): a state
+   loaded into a register a row ahead would be copied between registers by the compiler
+   at the loop's back edge, i.e. waited for right after its load was issued */
+__device__ __forceinline__ void lst_cp8(uint32_t dst, const void* src)
+{
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
 }
 
 __device__ __forceinline__ uint64_t lds_u64(uint32_t a)
@@ -118,7 +127,9 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ 
     const uint32_t after = tab + LST_TAB;
     const uint32_t yf_sh = after + ((uint32_t)NW - na) * LST_RING;
     const uint32_t jump_sh = yf_sh + NL * 8;
-    if (jump_sh + 16u * (TMA_K + 1) > base + dyn) {
+    /* per thread 16 bytes: the next row's state (and gamma) */
+    const uint32_t stslot = ((jump_sh + 16u * (TMA_K + 1) + 15u) & ~15u) + (uint32_t)threadIdx.x * 16u;
+    if (stslot + 16u * (NW * 32 - threadIdx.x) > base + dyn) {
         if (threadIdx.x == 0) gz_raise(GZ_ERR_CHECK, __LINE__);
         return;
     }
@@ -159,7 +170,6 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ 
     int k = -1;
     bool valid = false, failed = false;
     uint64_t S = 0, gam = 0;
-    uint64_t S_next = 0, gam_next = 0;   /* the next row's state, loaded a row ahead */
     uint32_t C = 0;          /* deviates committed by this lane (all rows) */
     uint32_t c_row0 = 0;     /* C at the start of the current row */
     uint32_t c_rowend = 0;   /* C at its end */
@@ -180,14 +190,20 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ 
     uint32_t sid = g0 * 32 + (uint32_t)lane - sstride;   /* modular: the first row adds sstride back */
     const int64_t rstride = (int64_t)sstride * p.ld;
     double* rowp = p.out + (int64_t)(g0 * 32 + (uint32_t)lane) * p.ld - rstride;
-    auto load_state = [&](uint32_t q, uint64_t& s, uint64_t& g) {
-        q = min(q, last);   /* clamped: the load is unconditional */
+    auto prefetch_state = [&](uint32_t q) {
+        q = min(q, last);   /* clamped: the copy is unconditional */
         if constexpr (SRC == 0) {
-            s = ld_keep(p.state_in + q);
+            lst_cp8(stslot, p.state_in + q);
         } else {
-            s = ld_keep(p.state_in + 2 * (int64_t)q);
-            g = ld_keep(p.state_in + 2 * (int64_t)q + 1);
+            lst_cp8(stslot, p.state_in + 2 * (int64_t)q);
+            lst_cp8(stslot + 8, p.state_in + 2 * (int64_t)q + 1);
         }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    auto take_state = [&](uint64_t& s, uint64_t& g) {
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        s = lds_u64(stslot);
+        if constexpr (SRC == 1) g = lds_u64(stslot + 8);
     };
     /* the row transition (divergent: once per row and lane, called when C >= c_rowend and
        k < ng): finish the row, start the next (at most one per round) */
@@ -231,9 +247,8 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ 
             sid += sstride;
             rowp += rstride;
             valid = k < ng && sid < n_streams;
-            S = S_next;
-            gam = gam_next;
-            load_state(sid + sstride, S_next, gam_next);
+            take_state(S, gam);
+            prefetch_state(sid + sstride);
             c_rowend = valid ? C + rowlen : C;   /* no stream: skip the row */
             if constexpr (MUT) {
                 if (valid) {
@@ -245,7 +260,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ 
             }
         }
     };
-    if (ng > 0) load_state(sid + sstride, S_next, gam_next);
+    if (ng > 0) prefetch_state(sid + sstride);
     next_row();
 
     while (__any_sync(GZ_FULL, k < ng)) {
