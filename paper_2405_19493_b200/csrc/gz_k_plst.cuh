@@ -37,7 +37,7 @@ constexpr uint64_t PLST_NEAR1 = 0x3fee000000000000ULL;   /* glibc log's near-1 i
    (16 slots x 32 lanes x 8 B) and a near-1 queue of 32 K entries x 32 B */
 __host__ __device__ constexpr uint32_t plst_smem_bytes(int NW, int K)
 {
-    return 2048u + 16u * (uint32_t)(K + 1) + (uint32_t)NW * (LST_RING + 32u * 32u * (uint32_t)K) + 1024u;
+    return 2048u + 16u * (uint32_t)(K + 1) + (uint32_t)NW * (LST_RING + 32u * 32u * (uint32_t)K + 32u * 16u) + 1024u;
 }
 
 /* one u64 of the stream from the draw cursor (LCG48: bits 16..47 of two steps, the
@@ -86,6 +86,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_polar_lst(const __grid_constant_
     const uint32_t wsh = warps_sh + wib * (LST_RING + QB);
     const uint32_t ringl = wsh + (uint32_t)lane * 8;   /* staging slot s of this lane at ringl + 256 s */
     const uint32_t q_sh = wsh + LST_RING;             /* near-1 queue: {v1, v2, s, staging address} */
+    const uint32_t stslot = warps_sh + NW * (LST_RING + QB) + (uint32_t)threadIdx.x * 16u;   /* next row's state */
     const uint64_t inc1 = SRC == 0 ? ld_keep(&c_lcgC[1]) : 0, inc2 = SRC == 0 ? ld_keep(&c_lcgC[2]) : 0;
     const int n_per = p.n_per;
     const uint32_t guard32 = p.guard > 0xffffffffll ? 0xffffffffu : (uint32_t)p.guard;
@@ -97,7 +98,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_polar_lst(const __grid_constant_
 
     int k = -1;
     bool valid = false, failed = false;
-    uint64_t S = 0, gam = 0, S_next = 0, gam_next = 0;
+    uint64_t S = 0, gam = 0;
     uint32_t C = 0, c_row0 = 0, c_rowend = 0, f = 0;
     uint32_t rej = 0;
     int has = 0;          /* the finished row left a spare */
@@ -107,14 +108,21 @@ __global__ void __launch_bounds__(NW * 32, 1) k_polar_lst(const __grid_constant_
     uint32_t sid = g0 * 32 + (uint32_t)lane - sstride;
     const int64_t rstride = (int64_t)sstride * p.ld;
     double* rowp = p.out + (int64_t)(g0 * 32 + (uint32_t)lane) * p.ld - rstride;
-    auto load_state = [&](uint32_t q, uint64_t& s, uint64_t& g) {
+    /* the next row's state, copied global -> shared by cp.async (as k_zig_lst) */
+    auto prefetch_state = [&](uint32_t q) {
         q = min(q, last);
         if constexpr (SRC == 0) {
-            s = ld_keep(p.state_in + q);
+            lst_cp8(stslot, p.state_in + q);
         } else {
-            s = ld_keep(p.state_in + 2 * (int64_t)q);
-            g = ld_keep(p.state_in + 2 * (int64_t)q + 1);
+            lst_cp8(stslot, p.state_in + 2 * (int64_t)q);
+            lst_cp8(stslot + 8, p.state_in + 2 * (int64_t)q + 1);
         }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    auto take_state = [&](uint64_t& s, uint64_t& g) {
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        s = lds_u64(stslot);
+        if constexpr (SRC == 1) g = lds_u64(stslot + 8);
     };
     /* the row transition (divergent: once per row and lane) */
     auto next_row = [&]() {
@@ -145,9 +153,8 @@ __global__ void __launch_bounds__(NW * 32, 1) k_polar_lst(const __grid_constant_
         sid += sstride;
         rowp += rstride;
         valid = k < ng && sid < n_streams;
-        S = S_next;
-        gam = gam_next;
-        load_state(sid + sstride, S_next, gam_next);
+        take_state(S, gam);
+        prefetch_state(sid + sstride);
         c_rowend = valid ? C + (uint32_t)n_per : C;
         if (valid && n_per > 0 && p.has_in && p.has_in[sid]) {
             /* the cached deviate comes first (samplers.py:182-184) */
@@ -155,7 +162,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_polar_lst(const __grid_constant_
             C += 1;
         }
     };
-    if (ng > 0) load_state(sid + sstride, S_next, gam_next);
+    if (ng > 0) prefetch_state(sid + sstride);
     next_row();
 
     while (__any_sync(GZ_FULL, k < ng)) {
