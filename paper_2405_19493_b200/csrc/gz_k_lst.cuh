@@ -267,6 +267,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ 
         /* ---- one round: TMA_K attempts per lane, no branches ---- */
         const bool act = C < c_rowend;
         const uint32_t C0 = C;
+        GZ_CHECK(C0 - f <= 3u, C0 - f);   /* the unstored deviates sit at slots 0..2 */
         uint32_t fm = 0;
         /* the deviates stay in registers until the last attempt: a table gather may not
            pass a shared store in program order (ptxas cannot tell that they never alias) */
@@ -344,6 +345,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ 
         if (__any_sync(GZ_FULL, frozen)) {
             if (frozen) {
                 const uint32_t slot = ringl + (C - f) * 256;   /* the frozen attempt's staged x */
+                GZ_CHECK(C - f < (uint32_t)LST_SLOTS, C - f);
                 const uint64_t u = tma_recover<SRC>(S);
                 uint32_t i;
                 uint64_t m_unused, sgn;
@@ -387,6 +389,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ 
            back to slot 0 ---- */
         if (!failed) {
             const uint32_t pend = C - f;   /* <= K + 3 */
+            GZ_CHECK(pend <= (uint32_t)TMA_K + 3u, pend);
             double* dst = rowp + (MUT ? gpos : f - c_row0);
             uint32_t nst = 0;
 #pragma unroll

@@ -169,6 +169,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_polar_lst(const __grid_constant_
         /* ---- one round: K attempts per lane, no branches ---- */
         const bool act = C < c_rowend;
         const uint32_t C0 = C;
+        GZ_CHECK(C0 - f <= 3u, C0 - f);   /* the unstored deviates sit at slots 0..2 */
         const uint32_t wb = ringl + (C0 - f) * 256;   /* slot of deviate C0 */
         uint32_t sl = (uint32_t)S, sh = (uint32_t)(S >> 32);
         uint32_t am = 0, cnt = 0, qn = 0;
@@ -260,13 +261,16 @@ __global__ void __launch_bounds__(NW * 32, 1) k_polar_lst(const __grid_constant_
             __syncwarp();
         }
         /* the completed row's spare: the second output of its last pair */
+        GZ_CHECK(qn <= 32u * K, qn);
         if (row_spare) {
+            GZ_CHECK(c_rowend - f < (uint32_t)LST_SLOTS, c_rowend - f);
             has = 1;
             spare = __longlong_as_double((long long)lds_u64(ringl + (c_rowend - f) * 256));
         }
         /* ---- complete 4-deviate chunks to the row (slots 0, 4, 8, 12) ---- */
         if (!failed) {
             const uint32_t pend = C - f;   /* <= 2 K + 3 */
+            GZ_CHECK(pend <= 2u * K + 3u, pend);
             double* dst = rowp + (f - c_row0);
             uint32_t nst = 0;
 #pragma unroll
