@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ 
     /* LCG: (A, C) of 2n steps, n <= K (the state after n draws from a round's start) */
     if (SRC == 0 && threadIdx.x <= TMA_K)
         asm volatile("st.shared.v2.u64 [%0], {%1, %2};" ::"r"(jump_sh + 16 * threadIdx.x), "l"(c_lcgA[2 * threadIdx.x]),
-                     "l"(c_lcgC[2 * threadIdx.x])
+                     "l"(c_lcgC[2 * threadIdx.x] << 16)
                      : "memory");
     __syncthreads();
 
@@ -157,7 +157,10 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ 
     const uint32_t kwl = tab | ((uint32_t)(lane & 7) << 4);
     const int n_per = p.n_per;
     /* the increments of one and two LCG steps, C and A C + C, held in registers */
-    const uint64_t inc1 = SRC == 0 ? ld_keep(&c_lcgC[1]) : 0, inc2 = SRC == 0 ? ld_keep(&c_lcgC[2]) : 0;
+    /* LCG48 in the shifted domain: the lane keeps T = state * 2^16 mod 2^64, which obeys
+       T' = A T + (C << 16) mod 2^64, so a step's output bits 16..47 are T's high word --
+       no funnel shift -- and the jump, inverse and increments carry C << 16 */
+    const uint64_t inc1 = SRC == 0 ? ld_keep(&c_lcgC[1]) << 16 : 0, inc2 = SRC == 0 ? ld_keep(&c_lcgC[2]) << 16 : 0;
     const uint32_t guard32 = p.guard > 0xffffffffll ? 0xffffffffu : (uint32_t)p.guard;
     /* stream ids in 32 bits: n_streams < 2^31 (lst_eligible), so id + 2 * sstride < 2^32 */
     const uint32_t n_streams = (uint32_t)p.n_streams;
@@ -203,6 +206,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ 
     auto take_state = [&](uint64_t& s, uint64_t& g) {
         asm volatile("cp.async.wait_group 0;" ::: "memory");
         s = lds_u64(stslot);
+        if constexpr (SRC == 0) s <<= 16;
         if constexpr (SRC == 1) g = lds_u64(stslot + 8);
     };
     /* the row transition (divergent: once per row and lane, called when C >= c_rowend and
@@ -228,7 +232,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ 
                     }
                 }
                 if constexpr (SRC == 0) {
-                    p.state_out[sid] = S & GZ_MASK48;
+                    p.state_out[sid] = S >> 16;
                 } else {
                     asm volatile("st.global.v2.u64 [%0], {%1, %2};" ::"l"(p.state_out + 2 * (int64_t)sid), "l"(S), "l"(gam)
                                  : "memory");
@@ -284,8 +288,8 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ 
                 const uint64_t p2 = (uint64_t)sl * 0xB4600A69u + inc2;
                 t2l = (uint32_t)p2;
                 t2h = (uint32_t)(p2 >> 32) + sh * 0xB4600A69u + sl * 0xBB20u;
-                uhi = __funnelshift_r(t1l, t1h, 16);
-                ulo = __funnelshift_r(t2l, t2h, 16);
+                uhi = t1h;
+                ulo = t2h;
                 sl = t2l;
                 sh = t2h;
             } else {
@@ -346,7 +350,14 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ 
             if (frozen) {
                 const uint32_t slot = ringl + (C - f) * 256;   /* the frozen attempt's staged x */
                 GZ_CHECK(C - f < (uint32_t)LST_SLOTS, C - f);
-                const uint64_t u = tma_recover<SRC>(S);
+                uint64_t u;
+                if constexpr (SRC == 0) {
+                    /* the draw that produced T: the previous T by the inverse step mod 2^64 */
+                    const uint64_t t1 = (S - inc1) * 0x7B13DFE05BCB1365ULL;   /* A^-1 mod 2^64 */
+                    u = (t1 & 0xffffffff00000000ULL) | (S >> 32);
+                } else {
+                    u = tma_recover<SRC>(S);
+                }
                 uint32_t i;
                 uint64_t m_unused, sgn;
                 tma_split<MOD>(u, i, m_unused, sgn);
@@ -355,7 +366,14 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ 
                 if (i != 0) {
                     /* wedge: the next draw is its uniform, whatever the outcome; an accepted
                        wedge's slot already holds x */
-                    const uint64_t u2 = tma_draw<SRC>(S, gam);
+                    uint64_t u2;
+                    if constexpr (SRC == 0) {
+                        const uint64_t t1 = S * GZ_LCG_A + inc1, t2 = t1 * GZ_LCG_A + inc1;
+                        S = t2;
+                        u2 = (t1 & 0xffffffff00000000ULL) | (t2 >> 32);
+                    } else {
+                        u2 = tma_draw<SRC>(S, gam);
+                    }
                     ok = wedge_accept_f(u2, x, p.yd + i, lds_f32x2(yf_sh + 8 * i));
                     if (!ok) {
                         rej = (C == c_rej) ? rej + 1 : 1;   /* consecutive rejections */
@@ -367,8 +385,8 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ 
                         }
                     }
                 } else {
-                    const TailOut to = tail_seq<SRC>(S & (SRC == 0 ? GZ_MASK48 : ~0ULL), gam, p.r, p.guard);
-                    S = to.st;
+                    const TailOut to = tail_seq<SRC>(SRC == 0 ? S >> 16 : S, gam, p.r, p.guard);
+                    S = SRC == 0 ? to.st << 16 : to.st;
                     x = to.v;
                     ok = to.k >= 0;
                     if (ok) {
