@@ -40,8 +40,9 @@ __host__ __device__ constexpr uint32_t plst_smem_bytes(int NW, int K)
     return 2048u + 16u * (uint32_t)(K + 1) + (uint32_t)NW * (LST_RING + 32u * 32u * (uint32_t)K + 32u * 16u) + 1024u;
 }
 
-/* one u64 of the stream from the draw cursor (LCG48: bits 16..47 of two steps, the
-   second straight from the cursor by (A^2, AC + C); SplitMix64: t += gamma, mix64) */
+/* one u64 of the stream from the draw cursor (LCG48 in the shifted domain of k_zig_lst,
+   T = state << 16: bits 16..47 of a step are T's high word; two steps, the second
+   straight from the cursor by (A^2, AC + C); SplitMix64: t += gamma, mix64) */
 template <int SRC>
 __device__ __forceinline__ uint64_t plst_draw(uint32_t& sl, uint32_t& sh, uint64_t gam, uint64_t inc1, uint64_t inc2)
 {
@@ -53,7 +54,7 @@ __device__ __forceinline__ uint64_t plst_draw(uint32_t& sl, uint32_t& sh, uint64
         const uint32_t t2h = (uint32_t)(p2 >> 32) + sh * 0xB4600A69u + sl * 0xBB20u;
         sl = t2l;
         sh = t2h;
-        return ((uint64_t)__funnelshift_r(t1l, t1h, 16) << 32) | __funnelshift_r(t2l, t2h, 16);
+        return ((uint64_t)t1h << 32) | t2h;
     } else {
         const uint64_t t = (((uint64_t)sh << 32) | sl) + gam;
         sl = (uint32_t)t;
@@ -76,7 +77,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_polar_lst(const __grid_constant_
     /* LCG: (A, C) of 4n steps, n <= K (the state after n attempts from a round's start) */
     if (SRC == 0 && threadIdx.x <= K)
         asm volatile("st.shared.v2.u64 [%0], {%1, %2};" ::"r"(jump_sh + 16 * threadIdx.x), "l"(c_lcgA[4 * threadIdx.x]),
-                     "l"(c_lcgC[4 * threadIdx.x])
+                     "l"(c_lcgC[4 * threadIdx.x] << 16)
                      : "memory");
     __syncthreads();
 
@@ -87,7 +88,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_polar_lst(const __grid_constant_
     const uint32_t ringl = wsh + (uint32_t)lane * 8;   /* staging slot s of this lane at ringl + 256 s */
     const uint32_t q_sh = wsh + LST_RING;             /* near-1 queue: {v1, v2, s, staging address} */
     const uint32_t stslot = warps_sh + NW * (LST_RING + QB) + (uint32_t)threadIdx.x * 16u;   /* next row's state */
-    const uint64_t inc1 = SRC == 0 ? ld_keep(&c_lcgC[1]) : 0, inc2 = SRC == 0 ? ld_keep(&c_lcgC[2]) : 0;
+    const uint64_t inc1 = SRC == 0 ? ld_keep(&c_lcgC[1]) << 16 : 0, inc2 = SRC == 0 ? ld_keep(&c_lcgC[2]) << 16 : 0;
     const int n_per = p.n_per;
     const uint32_t guard32 = p.guard > 0xffffffffll ? 0xffffffffu : (uint32_t)p.guard;
     const uint32_t n_streams = (uint32_t)p.n_streams;   /* < 2^31 (plst_eligible) */
@@ -122,6 +123,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_polar_lst(const __grid_constant_
     auto take_state = [&](uint64_t& s, uint64_t& g) {
         asm volatile("cp.async.wait_group 0;" ::: "memory");
         s = lds_u64(stslot);
+        if constexpr (SRC == 0) s <<= 16;   /* the shifted domain */
         if constexpr (SRC == 1) g = lds_u64(stslot + 8);
     };
     /* the row transition (divergent: once per row and lane) */
@@ -133,7 +135,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_polar_lst(const __grid_constant_
                 /* the row's last partial chunk (slots 0 .. c_rowend - f - 1) */
                 for (uint32_t q = 0; q < c_rowend - f; ++q) rowp[f + q - c_row0] = __longlong_as_double((long long)lds_u64(ringl + 256 * q));
                 if constexpr (SRC == 0) {
-                    p.state_out[sid] = S & GZ_MASK48;
+                    p.state_out[sid] = S >> 16;
                 } else {
                     asm volatile("st.global.v2.u64 [%0], {%1, %2};" ::"l"(p.state_out + 2 * (int64_t)sid), "l"(S), "l"(gam)
                                  : "memory");
