@@ -104,7 +104,7 @@ __device__ __forceinline__ uint64_t mut_x(uint64_t x, double sig, uint64_t zb)
         __dadd_rn(__longlong_as_double((long long)x), __dmul_rn(sig, __longlong_as_double((long long)zb))));
 }
 
-/* (double)m for m = mhi * 2^32 + mlo < 2^56, rounded to nearest even */
+/* (double)m for m = mhi * 2^32 + mlo (< 2^56, or m * 512 < 2^64 for the modified ziggurat), rounded to nearest even */
 __device__ __forceinline__ double lst_u56_to_f64(uint32_t mhi, uint32_t mlo)
 {
     return __ull2double_rn(((uint64_t)mhi << 32) | mlo);
@@ -134,7 +134,14 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ 
         return;
     }
     for (int j = threadIdx.x; j < 256 * TMA_REP; j += blockDim.x) {
-        const ulonglong2 v = p.kw[(j / TMA_REP) & (NL - 1)];
+        ulonglong2 v = p.kw[(j / TMA_REP) & (NL - 1)];
+        if constexpr (MOD) {
+            /* the modified ziggurat's mantissa is u >> 9: with ktab << 9 and wtab * 2^-9 the
+               attempt compares and converts u & ~511 = m * 512 instead (m < k exactly when
+               m * 512 < k * 512; (double)(m * 512) * (w / 512) rounds as (double)m * w) */
+            v.x <<= 9;
+            v.y = (unsigned long long)__double_as_longlong(__dmul_rn(__longlong_as_double((long long)v.y), 0x1p-9));
+        }
         asm volatile("st.shared.v2.u64 [%0], {%1, %2};" ::"r"(tab + (uint32_t)(j / TMA_REP) * 256 + (uint32_t)(j % TMA_REP) * 16),
                      "l"(v.x), "l"(v.y)
                      : "memory");
@@ -303,8 +310,8 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ 
             uint32_t mhi, mlo, sgn, row;
             if constexpr (MOD) {
                 row = __byte_perm(ulo, kwl, 0x7604);   /* layer = low byte */
-                mlo = __funnelshift_r(ulo, uhi, 9);
-                mhi = uhi >> 9;
+                mlo = ulo & ~511u;                     /* m * 512 (see the table fill) */
+                mhi = uhi;
                 sgn = (ulo << 23) & 0x80000000u;
             } else {
                 row = __byte_perm(uhi, kwl, 0x7634);   /* sign and layer = top byte */
