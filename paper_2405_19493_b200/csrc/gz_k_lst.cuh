@@ -135,6 +135,11 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ 
     }
     for (int j = threadIdx.x; j < 256 * TMA_REP; j += blockDim.x) {
         ulonglong2 v = p.kw[(j / TMA_REP) & (NL - 1)];
+        if constexpr (!MOD) {
+            /* entries 128..255 are the same layers with the sign bit set: a negative wtab
+               there makes m * wtab the signed deviate (negation is exact) */
+            if (j / TMA_REP >= 128) v.y ^= 0x8000000000000000ULL;
+        }
         if constexpr (MOD) {
             /* the modified ziggurat's mantissa is u >> 9: with ktab << 9 and wtab * 2^-9 the
                attempt compares and converts u & ~511 = m * 512 instead (m < k exactly when
@@ -324,7 +329,8 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ 
             const uint64_t m = ((uint64_t)mhi << 32) | mlo;
             const double x = __dmul_rn(lst_u56_to_f64(mhi, mlo), __longlong_as_double((long long)wb));
             if (m < kk) fm |= 1u << kk2;
-            zbs[kk2] = (uint64_t)__double_as_longlong(x) ^ ((uint64_t)sgn << 32);
+            /* the original ziggurat's sign is in the table row (see the fill) */
+            zbs[kk2] = MOD ? (uint64_t)__double_as_longlong(x) ^ ((uint64_t)sgn << 32) : (uint64_t)__double_as_longlong(x);
         }
         const uint32_t wbase = ringl + (C0 - f) * 256;   /* slot of deviate C0 */
         if (act) {
