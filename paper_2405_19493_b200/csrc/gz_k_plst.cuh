@@ -63,6 +63,13 @@ __device__ __forceinline__ uint64_t plst_draw(uint32_t& sl, uint32_t& sh, uint64
     }
 }
 
+/* v = 2 next_f64_unit() - 1 = (u >> 11) 2^-52 - 1, exact (samplers.py:185-186), computed as
+   (u & ~2047) 2^-63 - 1: the same 53-bit integer scaled, one mask instead of a 64-bit shift */
+__device__ __forceinline__ double plst_pm1(uint64_t u)
+{
+    return __fma_rn(__ull2double_rn(u & ~2047ULL), 0x1p-63, -1.0);
+}
+
 template <int SRC, int NW, int K>
 __global__ void __launch_bounds__(NW * 32, 1) k_polar_lst(const __grid_constant__ LaneParams p)
 {
@@ -177,8 +184,8 @@ __global__ void __launch_bounds__(NW * 32, 1) k_polar_lst(const __grid_constant_
         uint32_t am = 0, cnt = 0, qn = 0;
 #pragma unroll
         for (int j = 0; j < K; ++j) {
-            const double v1 = gz_unit53_pm1(plst_draw<SRC>(sl, sh, gam, inc1, inc2));
-            const double v2 = gz_unit53_pm1(plst_draw<SRC>(sl, sh, gam, inc1, inc2));
+            const double v1 = plst_pm1(plst_draw<SRC>(sl, sh, gam, inc1, inc2));
+            const double v2 = plst_pm1(plst_draw<SRC>(sl, sh, gam, inc1, inc2));
             const double s = __dadd_rn(__dmul_rn(v1, v1), __dmul_rn(v2, v2));
             const uint64_t sb = (uint64_t)__double_as_longlong(s);
             const bool acc = s > 0.0 && s < 1.0;
