@@ -783,10 +783,13 @@ def test_abi_rejects_bad_arguments_and_recovers():
 
 @pytest.mark.parametrize("source,alg", [("splitmix", "ziggurat"), ("lcg48", "ziggurat"),
                                         ("splitmix", "modified-ziggurat"), ("lcg48", "modified-ziggurat")])
-def test_few_long_streams_segmented_vs_oracle(source, alg):
+@pytest.mark.parametrize("pos", ["0", "1"])
+def test_few_long_streams_segmented_vs_oracle(source, alg, pos, monkeypatch):
     """Fewer streams than the GPU holds warps: G warps per stream decode speculative
-    segments (gz_k_seg.cuh) -- values and final states equal the oracle's for row
-    lengths around the segment sizes and stream counts up to one wave."""
+    segments (gz_k_seg.cuh; pos=1: the position decode, gz_k_pos.cuh) -- values and final
+    states equal the oracle's for row lengths around the segment sizes and stream counts
+    up to one wave."""
+    monkeypatch.setenv("GZ_POS", pos)
     for n, n_per in ((1, 512), (1, 20000), (2, 700), (7, 4096), (300, 513), (1024, 4096), (1100, 600)):
         rng = np.random.default_rng(zlib.crc32(f"seg/{source}/{alg}/{n}/{n_per}".encode()))
         if source == "lcg48":
@@ -801,11 +804,14 @@ def test_few_long_streams_segmented_vs_oracle(source, alg):
         assert np.array_equal(u64(st).reshape(ref_st.shape), ref_st), (n, n_per)
 
 
-@pytest.mark.parametrize("knob", ["GZ_SEG_GUESS=1", "GZ_SEG_FALLBACK=1", "GZ_SEG=0"])
+@pytest.mark.parametrize("knob", ["GZ_SEG_GUESS=1", "GZ_SEG_FALLBACK=1", "GZ_POS=1", "GZ_POS=1,GZ_POS_FALLBACK=1",
+                                  "GZ_POS=1,GZ_POS_SERIAL=1", "GZ_SEG=0"])
 def test_segmented_redecode_and_fallback_paths(knob):
-    """The rare paths of the segmented decode, forced: every speculative segment
-    re-decoded from its true entry (wrong guesses), every stream handed to the exact
-    warp loop, and the path disabled -- all give the default run's bits."""
+    """The rare paths of the few-long-streams decodes, forced: the speculative segment
+    decode (k_zig_lseg, the default) with every segment re-decoded from its true entry
+    (wrong guesses) or every stream handed to the exact warp loop; the position decode
+    (k_zig_pos, GZ_POS=1) as it runs, handing every stream to the exact loop, or parsing
+    every chunk sequentially; and both paths disabled -- all give the default run's bits."""
     import os
     import subprocess
     import sys
@@ -825,16 +831,65 @@ print(repr(res))
     outs = []
     for env_kv in ("", knob):
         env = dict(os.environ)
-        for k in ("GZ_SEG", "GZ_SEG_GUESS", "GZ_SEG_FALLBACK"):
+        for k in ("GZ_SEG", "GZ_SEG_GUESS", "GZ_SEG_FALLBACK", "GZ_POS", "GZ_POS_FALLBACK", "GZ_POS_SERIAL"):
             env.pop(k, None)
-        if env_kv:
-            k, v = env_kv.split("=")
+        for kv in filter(None, env_kv.split(",")):
+            k, v = kv.split("=")
             env[k] = v
         r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
                            cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
         assert r.returncode == 0, r.stderr[-2000:]
         outs.append(r.stdout.strip().splitlines()[-1])
     assert outs[0] == outs[1]
+
+
+@pytest.mark.parametrize("source,alg", [("splitmix", "ziggurat"), ("lcg48", "ziggurat"),
+                                        ("splitmix", "modified-ziggurat"), ("lcg48", "modified-ziggurat")])
+def test_position_decode_many_passes_and_strides(source, alg, monkeypatch):
+    """k_zig_pos over rows of many passes (2176 positions per full pass; the last pass
+    sized to the remaining deviates), row lengths around the pass sizes, strided rows
+    (ld > n_per, the padding left untouched), and a second call continuing the states."""
+    monkeypatch.setenv("GZ_POS", "1")
+    for n, n_per, pad in ((3, 100003, 0), (64, 2093, 5), (129, 2300, 1), (40, 4352, 0), (5, 65536, 3)):
+        rng = np.random.default_rng(zlib.crc32(f"pos/{source}/{alg}/{n}/{n_per}".encode()))
+        if source == "lcg48":
+            st_np = rng.integers(0, 2 ** 48, size=n, dtype=np.uint64)
+        else:
+            st_np = rng.integers(0, 2 ** 63, size=(n, 2), dtype=np.uint64) | np.uint64(1)
+        st = dev_states(source, st_np)
+        full = torch.full((n, n_per + pad), 7.0, dtype=torch.float64, device=DEV)
+        out = full[:, :n_per]
+        ref_st = st_np
+        for call in range(2):
+            streams.fill_gaussians_streams(alg, source, st, out)
+            ref, ref_st, *_ = O.fill_gaussians(alg, source, ref_st, n_per)
+            assert bits_equal(out.cpu().numpy(), ref), (n, n_per, call)
+            assert np.array_equal(u64(st).reshape(ref_st.shape), ref_st), (n, n_per, call)
+        if pad:
+            assert (full[:, n_per:] == 7.0).all()
+
+
+@pytest.mark.parametrize("guard", [1, 2, 3, 5, 40])
+def test_position_decode_small_guards(guard, monkeypatch):
+    """Guard trips under the position decode: the parse counts consecutive rejections
+    across passes and hands a tripping stream to the exact loop, which raises the
+    status; the status and the streams that do not trip equal the oracle's."""
+    monkeypatch.setenv("GZ_POS", "1")
+    n, n_per = 200, 3000
+    for source, alg in (("splitmix", "ziggurat"), ("lcg48", "modified-ziggurat")):
+        st_np = O.config_states("c1" if source == "splitmix" else "c4", range(n))
+        st = dev_states(source, st_np)
+        out = torch.empty((n, n_per), dtype=torch.float64, device=DEV)
+        ref, ref_st, _, _, status = O.fill_gaussians(alg, source, st_np, n_per, guard=guard)
+        try:
+            streams.fill_gaussians_streams(alg, source, st, out, guard=guard)
+            got = 0
+        except gz.RejectionLoopExceeded:
+            got = 1
+        assert got == status, (source, alg, guard)
+        if status == 0:
+            assert bits_equal(out.cpu().numpy(), ref)
+            assert np.array_equal(u64(st).reshape(ref_st.shape), ref_st)
 
 
 # ---- maximum sizes: one launch of more than 2^32 output elements ---------------
