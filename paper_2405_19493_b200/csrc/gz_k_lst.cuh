@@ -284,7 +284,10 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ 
         const bool act = C < c_rowend;
         const uint32_t C0 = C;
         GZ_CHECK(C0 - f <= 3u, C0 - f);   /* the unstored deviates sit at slots 0..2 */
-        uint32_t fm = 0;
+        /* the leading fast accepts, counted as they come: the running AND rides in the
+           compare's predicate slot, the count is one predicated add per attempt */
+        bool fast = true;
+        uint32_t lead = 0;
         /* the deviates stay in registers until the last attempt: a table gather may not
            pass a shared store in program order (ptxas cannot tell that they never alias) */
         uint64_t zbs[TMA_K];
@@ -297,9 +300,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ 
                    (engine.py:52-58: bits 16..47 of each state) */
                 uint32_t t1l, t1h, t2l, t2h;
                 lcg_step32(sl, sh, t1l, t1h, inc1);
-                const uint64_t p2 = (uint64_t)sl * 0xB4600A69u + inc2;
-                t2l = (uint32_t)p2;
-                t2h = (uint32_t)(p2 >> 32) + sh * 0xB4600A69u + sl * 0xBB20u;
+                lcg_step32x2(sl, sh, t2l, t2h, inc2);
                 uhi = t1h;
                 ulo = t2h;
                 sl = t2l;
@@ -328,7 +329,10 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ 
             lds_tab(row, kk, wb);
             const uint64_t m = ((uint64_t)mhi << 32) | mlo;
             const double x = __dmul_rn(lst_u56_to_f64(mhi, mlo), __longlong_as_double((long long)wb));
-            if (m < kk) fm |= 1u << kk2;
+            fast = fast && m < kk;
+            /* (spelled as a predicated add: from `lead += fast` the compiler makes an add
+               and a predicated move) */
+            asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\t@q add.u32 %0, %0, 1;\n\t}" : "+r"(lead) : "r"((uint32_t)fast));
             /* the original ziggurat's sign is in the table row (see the fill) */
             zbs[kk2] = MOD ? (uint64_t)__double_as_longlong(x) ^ ((uint64_t)sgn << 32) : (uint64_t)__double_as_longlong(x);
         }
@@ -340,10 +344,9 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ 
         }
         bool frozen = false;
         if (act) {
-            const int lead = __ffs(~fm) - 1;   /* leading fast accepts */
-            const uint32_t C_lead = C0 + (uint32_t)lead;
+            const uint32_t C_lead = C0 + lead;
             C = min(C_lead, c_rowend);
-            frozen = C_lead < c_rowend && lead < TMA_K;
+            frozen = C_lead < c_rowend && lead < (uint32_t)TMA_K;
         }
         /* the live attempts are a prefix of the round: the committed ones plus a frozen
            one; the state after them by jump-ahead from the round's start */

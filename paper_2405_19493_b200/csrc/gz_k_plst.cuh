@@ -49,9 +49,8 @@ __device__ __forceinline__ uint64_t plst_draw(uint32_t& sl, uint32_t& sh, uint64
     if constexpr (SRC == 0) {
         uint32_t t1l, t1h;
         lcg_step32(sl, sh, t1l, t1h, inc1);
-        const uint64_t p2 = (uint64_t)sl * 0xB4600A69u + inc2;
-        const uint32_t t2l = (uint32_t)p2;
-        const uint32_t t2h = (uint32_t)(p2 >> 32) + sh * 0xB4600A69u + sl * 0xBB20u;
+        uint32_t t2l, t2h;
+        lcg_step32x2(sl, sh, t2l, t2h, inc2);
         sl = t2l;
         sh = t2h;
         return ((uint64_t)t1h << 32) | t2h;

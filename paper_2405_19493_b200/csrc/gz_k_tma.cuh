@@ -153,11 +153,32 @@ __device__ __forceinline__ void tma_split(uint64_t u, uint32_t& i, uint64_t& m, 
 /* one LCG48 step on 32-bit halves, (h:l) <- A*(h:l) + C mod 2^64 (only bits 0..47
    matter): IMAD.WIDE.U32 of the low words with the increment, two IMADs for the
    cross terms (A = 0x5_DEECE66D) */
+/* The cross terms ride on the product's high word as a chain of two IMADs (mad.lo.u32
+   spelled out, the halves taken by a register-pair move): written as a sum, the compiler
+   computes them beside the wide product and joins the two with an extra 3-input add on
+   the ALU pipe (8 instructions per two steps instead of 6). */
+__device__ __forceinline__ uint32_t mad_lo32(uint32_t a, uint32_t b, uint32_t c)
+{
+    uint32_t r;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+    return r;
+}
+__device__ __forceinline__ void u64_halves(uint64_t v, uint32_t& lo, uint32_t& hi)
+{
+    asm("mov.b64 {%0, %1}, %2;" : "=r"(lo), "=r"(hi) : "l"(v));
+}
 __device__ __forceinline__ void lcg_step32(uint32_t l, uint32_t h, uint32_t& ol, uint32_t& oh, uint64_t inc)
 {
-    const uint64_t p = (uint64_t)l * 0xDEECE66Du + inc;
-    ol = (uint32_t)p;
-    oh = (uint32_t)(p >> 32) + h * 0xDEECE66Du + l * 5u;
+    uint32_t ph;
+    u64_halves((uint64_t)l * 0xDEECE66Du + inc, ol, ph);
+    oh = mad_lo32(l, 5u, mad_lo32(h, 0xDEECE66Du, ph));
+}
+/* two steps at once, (A^2, A C + C): the same shape */
+__device__ __forceinline__ void lcg_step32x2(uint32_t l, uint32_t h, uint32_t& ol, uint32_t& oh, uint64_t inc2)
+{
+    uint32_t ph;
+    u64_halves((uint64_t)l * 0xB4600A69u + inc2, ol, ph);
+    oh = mad_lo32(l, 0xBB20u, mad_lo32(h, 0xB4600A69u, ph));
 }
 
 /* the draw cursor of one round.  LCG48: 32-bit halves of the unmasked state (bits
@@ -178,9 +199,7 @@ struct TmaCursor {
             lcg_step32(lo, hi, t1l, t1h, gam);   /* gam carries the increment 0xB for the LCG */
             /* the second state straight from the first (A^2, A*C + C): the two steps
                do not wait for each other */
-            const uint64_t p2 = (uint64_t)lo * 0xB4600A69u + inc2;
-            t2l = (uint32_t)p2;
-            t2h = (uint32_t)(p2 >> 32) + hi * 0xB4600A69u + lo * 0xBB20u;
+            lcg_step32x2(lo, hi, t2l, t2h, inc2);
             uhi = __funnelshift_r(t1l, t1h, 16);
             ulo = __funnelshift_r(t2l, t2h, 16);
             lo = t2l;
