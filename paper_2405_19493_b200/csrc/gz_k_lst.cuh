@@ -63,7 +63,8 @@ constexpr uint32_t LST_TAB = 0x10000;               /* the layer-row table (64 K
 __host__ __device__ constexpr uint32_t lst_smem_bytes(int NW, int NL, int K, uint32_t base = 0x400)
 {
     const uint32_t tab = (base + 0xFFFFu) & ~0xFFFFu;
-    const uint32_t na = (tab - base) / LST_RING < (uint32_t)NW ? (tab - base) / LST_RING : (uint32_t)NW;
+    const uint32_t r0 = (base + LST_RING - 1u) & ~(LST_RING - 1u);   /* rings are 4 KiB aligned */
+    const uint32_t na = (tab - r0) / LST_RING < (uint32_t)NW ? (tab - r0) / LST_RING : (uint32_t)NW;
     return tab + LST_TAB + ((uint32_t)NW - na) * LST_RING + (uint32_t)NL * 8 + 16u * (uint32_t)(K + 1) + 16u +
            (uint32_t)NW * 32u * 16u - base;
 }
@@ -85,6 +86,14 @@ __device__ __forceinline__ uint64_t lds_u64(uint32_t a)
 __device__ __forceinline__ void sts_u64(uint32_t a, uint64_t v)
 {
     asm volatile("st.shared.u64 [%0], %1;" ::"r"(a), "l"(v) : "memory");
+}
+
+/* the staging slot of deviate d of a lane (d counts the lane's deviates over all its rows):
+   slot d mod 16 of the lane's column.  The warp's staging block is 4 KiB aligned, so the
+   slot number is bits 8..11 of the address: one AND-OR on (d << 8). */
+__device__ __forceinline__ uint32_t lst_slot(uint32_t ringl, uint32_t d256)
+{
+    return ringl | (d256 & (LST_RING - 256u));
 }
 
 #ifndef LST_XPF
@@ -123,7 +132,8 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ 
     asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
     /* the layout of lst_smem_bytes from the real window offset */
     const uint32_t tab = (base + 0xFFFFu) & ~0xFFFFu;
-    const uint32_t na = min((uint32_t)NW, (tab - base) / LST_RING);
+    const uint32_t r0 = (base + LST_RING - 1u) & ~(LST_RING - 1u);
+    const uint32_t na = min((uint32_t)NW, (tab - r0) / LST_RING);
     const uint32_t after = tab + LST_TAB;
     const uint32_t yf_sh = after + ((uint32_t)NW - na) * LST_RING;
     const uint32_t jump_sh = yf_sh + NL * 8;
@@ -165,7 +175,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ 
     const int lane = threadIdx.x & 31;
     const uint32_t wib = threadIdx.x >> 5;
     /* the lane's staging column (slot s at ringl + 256 s) and its replica of the layer rows */
-    const uint32_t ringl = (wib < na ? base + wib * LST_RING : after + (wib - na) * LST_RING) + (uint32_t)lane * 8;
+    const uint32_t ringl = (wib < na ? r0 + wib * LST_RING : after + (wib - na) * LST_RING) + (uint32_t)lane * 8;
     const uint32_t kwl = tab | ((uint32_t)(lane & 7) << 4);
     const int n_per = p.n_per;
     /* the increments of one and two LCG steps, C and A C + C, held in registers */
@@ -229,7 +239,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ 
                 if (n_per & 3) {
                     /* the row's last partial chunk (slots 0 .. c_rowend - f - 1) */
                     for (uint32_t q = 0; q < c_rowend - f; ++q) {
-                        const uint64_t v = lds_u64(ringl + 256 * q);
+                        const uint64_t v = lds_u64(lst_slot(ringl, (f + q) << 8));
                         rowp[f + q - c_row0] = __longlong_as_double((long long)v);
                         if constexpr (STATS) tma_fold(v, ck, a1, a2, a3, a4);
                     }
@@ -336,11 +346,11 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ 
             /* the original ziggurat's sign is in the table row (see the fill) */
             zbs[kk2] = MOD ? (uint64_t)__double_as_longlong(x) ^ ((uint64_t)sgn << 32) : (uint64_t)__double_as_longlong(x);
         }
-        const uint32_t wbase = ringl + (C0 - f) * 256;   /* slot of deviate C0 */
+        const uint32_t c0s = C0 << 8;   /* deviate C0 + j goes to slot (C0 + j) mod 16 */
         if (act) {
 #pragma unroll
             for (int kk2 = 0; kk2 < TMA_K; ++kk2)
-                asm volatile("st.shared.u64 [%0], %1;" ::"r"(wbase + 256 * kk2), "l"(zbs[kk2]) : "memory");
+                asm volatile("st.shared.u64 [%0], %1;" ::"r"(lst_slot(ringl, c0s + 256u * kk2)), "l"(zbs[kk2]) : "memory");
         }
         bool frozen = false;
         if (act) {
@@ -364,7 +374,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ 
         /* ---- the frozen lanes' slow attempts, resolved together ---- */
         if (__any_sync(GZ_FULL, frozen)) {
             if (frozen) {
-                const uint32_t slot = ringl + (C - f) * 256;   /* the frozen attempt's staged x */
+                const uint32_t slot = lst_slot(ringl, C << 8);   /* the frozen attempt's staged x */
                 GZ_CHECK(C - f < (uint32_t)LST_SLOTS, C - f);
                 uint64_t u;
                 if constexpr (SRC == 0) {
@@ -429,7 +439,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ 
 #pragma unroll
             for (int q = 0; q < (TMA_K + 3) / 4; ++q) {
                 if (pend >= 4u * (q + 1)) {
-                    const uint32_t ph = ringl + 1024u * q;
+                    const uint32_t ph = lst_slot(ringl, (f << 8) + 1024u * q);   /* f is a multiple of 4: no wrap inside a chunk */
                     uint64_t v0 = lds_u64(ph), v1 = lds_u64(ph + 256), v2 = lds_u64(ph + 512), v3 = lds_u64(ph + 768);
                     if constexpr (MUT) {
                         /* x + sigma z (gaussian_affine with mu = x: two roundings) */
@@ -454,12 +464,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ 
                 }
             }
             if (nst != 0) {
-                const uint32_t ph = ringl + 1024u * nst;
-                const uint64_t w0 = lds_u64(ph), w1 = lds_u64(ph + 256), w2 = lds_u64(ph + 512);
-                sts_u64(ringl, w0);
-                sts_u64(ringl + 256, w1);
-                sts_u64(ringl + 512, w2);
-                f += 4u * nst;
+                f += 4u * nst;   /* the <= 3 left over stay where they are: slots f mod 16 .. */
                 if constexpr (MUT) {
                     gpos += 4u * nst;
                     if (gpos >= (uint32_t)n_per) gpos -= (uint32_t)n_per;
