@@ -29,10 +29,17 @@
  *  - staging: per warp 16 slots x 32 lanes x 8 bytes, slot-major (slot s of lane
  *    l at s * 256 + l * 8), so every lane owns one bank pair and the per-slot
  *    stores and chunk loads of a half-warp never conflict whatever the lanes'
- *    positions.  A lane's unstored deviates always start at slot 0: a round
- *    writes its K candidates at slots L .. L + K - 1 (L <= 3 unstored), complete
- *    4-deviate chunks leave from slots 0, 4, 8 with one 32-byte store each
- *    (STG.E.256: a full L2 sector), and the <= 3 left over move back to slot 0.
+ *    positions.  The slots are a ring: deviate d of a lane (counted over all its
+ *    rows) sits at slot d mod 16; the warp's block is 4 KiB aligned, so the slot
+ *    number is bits 8..11 of the address and a slot address is one AND-OR on
+ *    d << 8.  A round writes its K candidates behind the <= 3 unstored deviates,
+ *    complete 4-deviate chunks leave with one 32-byte store each (STG.E.256: a
+ *    full L2 sector; a chunk starts at a multiple of 4, so it never wraps), and
+ *    what is left over stays where it is.  (Until round 2's last pass the
+ *    unstored deviates were moved back to slot 0 every round: 3 loads and 3
+ *    stores per lane -- ncu showed the L1TEX LSU data pipe, which carries the
+ *    shared-memory wavefronts AND the lane-private sector stores, at 93.7 % of
+ *    its peak, so those 12 wavefronts per round were worth 4 % of the kernel.)
  *    Lanes never wait for each other: no warp-wide flush, no cross-lane drift.
  * Rows of a lane follow each other (lane l of warp g takes the streams
  * (g + k * warps) * 32 + l); the next row's state is loaded when a row starts.
@@ -126,6 +133,9 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ 
     constexpr bool MUT = EPI == EPI_MUTATE;
     static_assert(!MUT || (!STATS && TMA_K <= 8), "the mutation keeps the x of two chunks in registers");
     constexpr int NL = MOD ? 256 : 128;
+    /* the mutation epilogue keeps the first unstored deviate at slot 0 (it waits on the x
+       loads, not on the LSU pipe: the ring's address arithmetic cost it 1.5 %) */
+    constexpr bool RING = !MUT;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     const uint32_t base = sh_addr(smem_raw);
     uint32_t dyn;
@@ -239,7 +249,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ 
                 if (n_per & 3) {
                     /* the row's last partial chunk (slots 0 .. c_rowend - f - 1) */
                     for (uint32_t q = 0; q < c_rowend - f; ++q) {
-                        const uint64_t v = lds_u64(lst_slot(ringl, (f + q) << 8));
+                        const uint64_t v = lds_u64(lst_slot(ringl, (f + q) << 8));   /* (never a mutation row: genes % 4 == 0) */
                         rowp[f + q - c_row0] = __longlong_as_double((long long)v);
                         if constexpr (STATS) tma_fold(v, ck, a1, a2, a3, a4);
                     }
@@ -346,11 +356,13 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ 
             /* the original ziggurat's sign is in the table row (see the fill) */
             zbs[kk2] = MOD ? (uint64_t)__double_as_longlong(x) ^ ((uint64_t)sgn << 32) : (uint64_t)__double_as_longlong(x);
         }
-        const uint32_t c0s = C0 << 8;   /* deviate C0 + j goes to slot (C0 + j) mod 16 */
+        const uint32_t c0s = (RING ? C0 : C0 - f) << 8;   /* deviate C0 + j goes to slot (C0 + j) mod 16 */
         if (act) {
 #pragma unroll
             for (int kk2 = 0; kk2 < TMA_K; ++kk2)
-                asm volatile("st.shared.u64 [%0], %1;" ::"r"(lst_slot(ringl, c0s + 256u * kk2)), "l"(zbs[kk2]) : "memory");
+                asm volatile("st.shared.u64 [%0], %1;" ::"r"(RING ? lst_slot(ringl, c0s + 256u * kk2) : ringl + c0s + 256u * kk2),
+                             "l"(zbs[kk2])
+                             : "memory");
         }
         bool frozen = false;
         if (act) {
@@ -374,7 +386,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ 
         /* ---- the frozen lanes' slow attempts, resolved together ---- */
         if (__any_sync(GZ_FULL, frozen)) {
             if (frozen) {
-                const uint32_t slot = lst_slot(ringl, C << 8);   /* the frozen attempt's staged x */
+                const uint32_t slot = RING ? lst_slot(ringl, C << 8) : ringl + ((C - f) << 8);   /* the frozen attempt's staged x */
                 GZ_CHECK(C - f < (uint32_t)LST_SLOTS, C - f);
                 uint64_t u;
                 if constexpr (SRC == 0) {
@@ -439,7 +451,8 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ 
 #pragma unroll
             for (int q = 0; q < (TMA_K + 3) / 4; ++q) {
                 if (pend >= 4u * (q + 1)) {
-                    const uint32_t ph = lst_slot(ringl, (f << 8) + 1024u * q);   /* f is a multiple of 4: no wrap inside a chunk */
+                    /* f is a multiple of 4: no wrap inside a chunk */
+                    const uint32_t ph = RING ? lst_slot(ringl, (f << 8) + 1024u * q) : ringl + 1024u * q;
                     uint64_t v0 = lds_u64(ph), v1 = lds_u64(ph + 256), v2 = lds_u64(ph + 512), v3 = lds_u64(ph + 768);
                     if constexpr (MUT) {
                         /* x + sigma z (gaussian_affine with mu = x: two roundings) */
@@ -464,7 +477,15 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ 
                 }
             }
             if (nst != 0) {
-                f += 4u * nst;   /* the <= 3 left over stay where they are: slots f mod 16 .. */
+                if constexpr (!RING) {
+                    /* the <= 3 left over move back to slot 0 */
+                    const uint32_t ph = ringl + 1024u * nst;
+                    const uint64_t w0 = lds_u64(ph), w1 = lds_u64(ph + 256), w2 = lds_u64(ph + 512);
+                    sts_u64(ringl, w0);
+                    sts_u64(ringl + 256, w1);
+                    sts_u64(ringl + 512, w2);
+                }
+                f += 4u * nst;   /* RING: the <= 3 left over stay where they are, slots f mod 16 .. */
                 if constexpr (MUT) {
                     gpos += 4u * nst;
                     if (gpos >= (uint32_t)n_per) gpos -= (uint32_t)n_per;
