@@ -28,8 +28,38 @@
 /* (A_n, C_n): state after n single LCG steps = A_n*s + C_n mod 2^48, stored in
  * __constant__ c_lcgA / c_lcgC (gz_engine.cu) for n < GZ_LCG_JUMP_MAX. */
 
+/* 32-bit multiply-add and register-pair moves spelled out, so that the cross terms of a
+   64-bit product ride on the wide product's high word as a chain of two IMADs: written as
+   a sum, the compiler computes them beside the product and joins the two with one more
+   add (4 instructions per 64 x 64 -> 64 multiply by a constant instead of 3). */
+__device__ __forceinline__ uint32_t mad_lo32(uint32_t a, uint32_t b, uint32_t c)
+{
+    uint32_t r;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+    return r;
+}
+__device__ __forceinline__ void u64_halves(uint64_t v, uint32_t& lo, uint32_t& hi)
+{
+    asm("mov.b64 {%0, %1}, %2;" : "=r"(lo), "=r"(hi) : "l"(v));
+}
+template <uint64_t CC>
+__device__ __forceinline__ uint64_t gz_mul64c(uint64_t z)
+{
+    constexpr uint32_t clo = (uint32_t)CC, chi = (uint32_t)(CC >> 32);
+    uint32_t zl, zh, pl, ph;
+    u64_halves(z, zl, zh);
+    u64_halves((uint64_t)zl * clo, pl, ph);
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "r"(pl), "r"(mad_lo32(zl, chi, mad_lo32(zh, clo, ph))));
+    return r;
+}
+
+/* sources.py:83-88 (mix64, the SplitMix64 finaliser) */
 __device__ __forceinline__ uint64_t gz_mix64(uint64_t z)
 {
+    /* plain products: with gz_mul64c (3 instead of 4 instructions each) config 3 ran 465
+       G/s against 481 -- the two multiplies are in series and the longer chain costs more
+       than the two instructions save */
     z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
     z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
     return z ^ (z >> 31);

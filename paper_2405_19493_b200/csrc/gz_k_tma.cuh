@@ -157,16 +157,7 @@ __device__ __forceinline__ void tma_split(uint64_t u, uint32_t& i, uint64_t& m, 
    spelled out, the halves taken by a register-pair move): written as a sum, the compiler
    computes them beside the wide product and joins the two with an extra 3-input add on
    the ALU pipe (8 instructions per two steps instead of 6). */
-__device__ __forceinline__ uint32_t mad_lo32(uint32_t a, uint32_t b, uint32_t c)
-{
-    uint32_t r;
-    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
-    return r;
-}
-__device__ __forceinline__ void u64_halves(uint64_t v, uint32_t& lo, uint32_t& hi)
-{
-    asm("mov.b64 {%0, %1}, %2;" : "=r"(lo), "=r"(hi) : "l"(v));
-}
+/* (mad_lo32 and u64_halves: gz_device.cuh) */
 __device__ __forceinline__ void lcg_step32(uint32_t l, uint32_t h, uint32_t& ol, uint32_t& oh, uint64_t inc)
 {
     uint32_t ph;
