@@ -212,6 +212,41 @@ def test_strided_rows_and_fused_witnesses(policy):
     np.testing.assert_allclose(ps.cpu().numpy(), ps_ref, rtol=1e-12, atol=1e-9)
 
 
+@pytest.mark.parametrize("source", ["lcg48", "splitmix"])
+@pytest.mark.parametrize("alg", ["ziggurat", "modified-ziggurat"])
+@pytest.mark.parametrize("n,n_per,ld,stats", [(40000, 255, 256, True), (33000, 17, 20, False), (32768, 3, 4, True),
+                                               (36000, 101, 104, False)])
+def test_zig_lst_odd_rows_strided(source, alg, n, n_per, ld, stats):
+    """k_zig_lst (the auto choice from 32768 streams when rows are 32-byte aligned and the
+    stride a multiple of 4) on rows whose length is NOT a multiple of 4: the last partial
+    chunk of a row leaves from the ring-addressed staging slots at the row transition, the
+    next row starts on a chunk boundary.  With and without the fused witnesses; bit-exact
+    against the oracle, the padding untouched (engine.py:75-151 per stream)."""
+    rng = np.random.default_rng(n + n_per)
+    if source == "lcg48":
+        st_np = rng.integers(0, 1 << 48, size=n, dtype=np.uint64)
+    else:
+        st_np = rng.integers(0, 1 << 63, size=(n, 2), dtype=np.uint64)
+        st_np[:, 1] |= np.uint64(1)
+    st = dev_states(source, st_np)
+    big = torch.full((n, ld), -7.0, dtype=torch.float64, device=DEV)
+    out = big[:, :n_per]
+    kw = {}
+    if stats:
+        kw = dict(checksum=torch.zeros(n, dtype=torch.int64, device=DEV),
+                  psum=torch.zeros((n, 4), dtype=torch.float64, device=DEV))
+    streams.fill_gaussians_streams(alg, source, st, out, **kw)
+    ref, ref_st, *_ = O.fill_gaussians(alg, source, st_np, n_per)
+    assert bits_equal(out.cpu().numpy(), ref)
+    assert (big[:, n_per:] == -7.0).all()
+    assert np.array_equal(u64(st).reshape(ref_st.shape), ref_st)
+    if stats:
+        ck_ref = np.bitwise_xor.reduce(ref.view(np.uint64), axis=1)
+        assert np.array_equal(u64(kw["checksum"]), ck_ref)
+        ps_ref = np.stack([ref.sum(1), (ref ** 2).sum(1), (ref ** 3).sum(1), (ref ** 4).sum(1)], 1)
+        np.testing.assert_allclose(kw["psum"].cpu().numpy(), ps_ref, rtol=1e-12, atol=1e-9)
+
+
 @pytest.mark.parametrize("n,n_per,ld", [(40000, 255, 256), (33000, 17, 20), (2011, 101, 104), (700, 3, 4)])
 def test_polar_lane_odd_rows_strided_with_spares(n, n_per, ld):
     """k_polar_lst (polar, a lane per stream; the auto choice from 32768 streams, policy
