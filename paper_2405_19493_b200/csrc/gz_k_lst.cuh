@@ -247,7 +247,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ 
         {
             if (valid && !failed) {
                 if (n_per & 3) {
-                    /* the row's last partial chunk (slots 0 .. c_rowend - f - 1) */
+                    /* the row's last partial chunk (deviates f .. c_rowend - 1 of the ring) */
                     for (uint32_t q = 0; q < c_rowend - f; ++q) {
                         const uint64_t v = lds_u64(lst_slot(ringl, (f + q) << 8));   /* (never a mutation row: genes % 4 == 0) */
                         rowp[f + q - c_row0] = __longlong_as_double((long long)v);
@@ -303,7 +303,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_zig_lst(const __grid_constant__ 
         /* ---- one round: TMA_K attempts per lane, no branches ---- */
         const bool act = C < c_rowend;
         const uint32_t C0 = C;
-        GZ_CHECK(C0 - f <= 3u, C0 - f);   /* the unstored deviates sit at slots 0..2 */
+        GZ_CHECK(C0 - f <= 3u, C0 - f);   /* at most 3 unstored deviates (ring: at slots f mod 16 ..; mutation: at slots 0..2) */
         /* the leading fast accepts, counted as they come: the running AND rides in the
            compare's predicate slot, the count is one predicated add per attempt */
         bool fast = true;

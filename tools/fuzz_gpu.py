@@ -21,6 +21,9 @@ from paper_2405_19493_b200 import _lib, streams
 from paper_2405_19493_b200.engine import table_slot
 from paper_2405_19493_b200.samplers import make_sampler
 
+DRY = False     # main(): replay a case's random draws without running it (GZ_FUZZ_SKIP=N skips the first N cases)
+LAST = ""       # the case being run, printed when it raises
+
 PAIRINGS = [(s, a) for s in ("lcg48", "splitmix") for a in ("polar", "ziggurat", "modified-ziggurat")]
 
 
@@ -48,6 +51,10 @@ def one_case(rng):
         kw = dict(spare=torch.from_numpy(sp.copy()).cuda(), has_spare=torch.from_numpy(hs.copy()).cuda())
     host = bool(rng.integers(2))      # host buffers through gz_fill_gaussians_host
     guard = 1_000_000 if rng.random() < 0.8 else int(rng.integers(1, 6))
+    global LAST
+    LAST = f"{source}/{alg} n={n} n_per={n_per} policy={policy} host={host} guard={guard}"
+    if DRY:
+        return 0
     tripped = False
     streams.set_kernel_policy(policy)
     try:
@@ -106,6 +113,10 @@ def mutate_case(rng):
     x = full[:, :genes]
     st = torch.from_numpy(st_np.view(np.int64).copy()).cuda()
     guard = 1_000_000 if rng.random() < 0.8 else int(rng.integers(1, 6))
+    global LAST
+    LAST = f"mutate n={n} genes={genes} gens={gens} pad={pad} policy={policy} guard={guard}"
+    if DRY:
+        return 0
     tripped = False
     streams.set_kernel_policy(policy)
     try:
@@ -131,6 +142,10 @@ def u64_case(rng):
                                                                           int(rng.integers(0, 300)))
     st_np = rng.integers(0, 2 ** 48, size=n, dtype=np.uint64) if source == "lcg48" else \
         rng.integers(0, 2 ** 63, size=(n, 2), dtype=np.uint64) | np.uint64(1)
+    global LAST
+    LAST = f"u64 {source} n={n} n_per={n_per}"
+    if DRY:
+        return 0
     st = torch.from_numpy(np.ascontiguousarray(st_np).view(np.int64).copy()).cuda()
     out = torch.empty((n, n_per), dtype=torch.int64, device="cuda")
     streams.fill_u64_streams(source, st, out)
@@ -146,12 +161,18 @@ def main():
     rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 12345)
     t_end = time.time() + secs
     cases = total = 0
+    skip = int(os.environ.get("GZ_FUZZ_SKIP", "0"))
+    global DRY
     while time.time() < t_end:
+        DRY = cases < skip
         try:
             k = rng.random()
             total += (one_case if k < 0.7 else mutate_case if k < 0.9 else u64_case)(rng)
         except AssertionError as e:
             print("MISMATCH", e, flush=True)
+            return 1
+        except Exception as e:  # noqa: BLE001 -- a CUDA error: say which case
+            print(f"ERROR in case {cases}: {LAST}: {e!r}", flush=True)
             return 1
         cases += 1
         if cases % 50 == 0:
